@@ -1,0 +1,322 @@
+"""bench.py — training throughput of the B200 PNN hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+A step is one pass of the whole hot path over the config's synthetic data:
+E epochs of per-sample SGD of every CN on its slice, the
+averaging merge incl. the cross-rank all-reduce (a7) and the test-set readout
+of the merged network (a8).  value = Σ_ranks K_local·S·E / max_ranks(step time).
+Scaling is strong: the config's K CNs and rows are split over the N ranks.
+
+--impl reference times the CPU oracle (oracle/, the deliberately slow
+single-threaded C trainer) on the host cores, on a bounded sample of the
+same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import CONFIGS  # noqa: E402
+
+METRIC = "training samples/sec (fwd+bwd+update, whole box)"
+
+
+def fma_per_sample(layers):
+    """Algorithmic FMAs per training sample: forward P,
+    hidden deltas P - P1, update P  →  3P - P1 (P = weights, P1 = |W^1|)."""
+    P = sum(layers[l] * layers[l - 1] for l in range(1, len(layers)))
+    P1 = layers[0] * layers[1]
+    return 3 * P - P1
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index=0, period=0.1):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # noqa: BLE001
+            self.error = str(e)
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for n, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "n_samples": len(self.samples)}
+
+
+def _oracle_sample(cfg, budget_s):
+    """Pick a bounded sample of the workload's CNs (≈budget_s of CPU work on
+    the host cores, ~1.2 GFLOP/s/core scalar fp32) and pre-generate its rows."""
+    import oracle
+    from datagen import make_rows
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    start, count = oracle.shard_bounds(cfg.n_train, cfg.K)
+    S = int(count[0])
+    per_cn = S * cfg.epochs * fma_per_sample(cfg.layers) * 2 / 1.0e9      # GFLOP per CN
+    n_cn = int(max(1, min(cfg.K, budget_s * 1.2 * cores / per_cn)))
+    if n_cn >= cores:
+        n_cn = (n_cn // cores) * cores
+    sample = list(range(n_cn))
+    data = {int(start[i]): make_rows(int(start[i]), int(count[i]), "train", 0) for i in sample}
+    threads = min(cores, n_cn)
+
+    def run():
+        oracle.train_pnn_rows(cfg.layers, cfg.act, cfg.init, cfg.K, cfg.lr, 0, cfg.n_train,
+                              lambda s, c: data[s], epochs=cfg.epochs, batch=cfg.batch,
+                              threads=threads, subnets=sample)
+
+    desc = (f"{n_cn} of {cfg.K} CNs x {S} rows x {cfg.epochs} epoch(s), batch {cfg.batch}: "
+            f"fp32 oracle, one CN per thread, {threads} threads; merge/readout not timed")
+    return run, n_cn * S * cfg.epochs, threads, desc
+
+
+def run_reference(args, cfg):
+    """The oracle, as it stands, on the host cores (bounded sample per step)."""
+    run, units, threads, desc = _oracle_sample(cfg, 4.0)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        run()
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    value = units / t
+    return {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": cfg.name, "layers": list(cfg.layers), "K": cfg.K,
+                   "rows": cfg.n_train, "epochs": cfg.epochs, "batch": cfg.batch},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def cpu_baseline(cfg, budget_s=12.0):
+    run, units, threads, desc = _oracle_sample(cfg, budget_s)
+    t0 = time.perf_counter()
+    run()
+    t = time.perf_counter() - t0
+    return {"value": units / t, "unit": "samples/s", "cores": threads, "kind": "oracle",
+            "sample": desc + f" ({t:.1f} s wall)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "reference", "resident"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, cfg)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from datagen import make_rows
+    from paper_2304_09590_b200 import PNN
+    from paper_2304_09590_b200.dist import nccl_unique_id_bytes, rank_rows, rank_subnets
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    first, K_local = rank_subnets(cfg.K, world, rank)
+    r0, nrows = rank_rows(cfg.n_train, cfg.K, world, rank)
+    X, y = make_rows(r0, nrows, "train", 0)
+    Xt, _ = make_rows(0, cfg.n_test, "test", 0)
+
+    net = PNN(cfg.layers, cfg.act, cfg.init, cfg.K, cfg.lr, seed=0)
+    net.set_kernel(args.kernel)
+    if cfg.batch > 1:
+        net.set_minibatch(cfg.batch)
+    if world > 1:
+        net.set_comm(world, rank, nccl_unique_id_bytes(rank))
+    kernel_id, _ = net.kernel_info()
+    xd = torch.from_numpy(X).cuda()
+    yd = torch.from_numpy(y).cuda()
+    xtd = torch.from_numpy(Xt).cuda()
+    labels = torch.empty(cfg.n_test, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(train_ev=None):
+        for _ in range(cfg.epochs):
+            if train_ev is not None:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            net.train_epoch(xd, yd, stream)
+            if train_ev is not None:
+                b.record(stream)
+                train_ev.append((a, b))
+        net.merge(stream)
+        net.predict(xtd, labels, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    train_ev = []
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(train_ev)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    train_ms = statistics.mean(a.elapsed_time(b) for a, b in train_ev)
+    t = torch.tensor([ms, train_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, train_ms = t.tolist()
+    units = cfg.n_train * cfg.epochs          # all ranks together (strong scaling)
+    value = units / (ms / 1e3)
+
+    # ---- end to end through the host-buffer C-ABI call ----------------------
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(X).pin_memory()
+        yh = torch.from_numpy(y).pin_memory()
+        xth = torch.from_numpy(Xt).pin_memory()
+        lab_h = torch.empty(cfg.n_test, dtype=torch.int32).pin_memory()
+
+        def step_host():
+            for _ in range(cfg.epochs):
+                net.train_epoch_host(xh, yh, stream)
+            net.merge(stream)
+            xtd.copy_(xth, non_blocking=True)
+            net.predict(xtd, labels, stream=stream)
+            lab_h.copy_(labels, non_blocking=True)
+
+        for _ in range(max(1, args.warmup // 2)):
+            step_host()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_host()
+        e1.record(stream)
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": units / (ems.item() / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": int(cfg.epochs * (X.nbytes + y.nbytes) + Xt.nbytes),
+               "d2h_bytes_per_step": int(lab_h.numel() * 4), "ms_per_step": ems.item()}
+
+    if rank == 0:
+        pk = peaks()
+        clocks = clk.summary()
+        sm_mhz = clocks["sm_mhz"] or pk.get("sm_max_mhz", 1965.0)
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        flop_launch = 2.0 * fma_per_sample(cfg.layers) * (nrows)   # this rank's launch
+        achieved = flop_launch / (train_ms / 1e3) / 1e12
+        peak_max = sms * 128 * 2 * (pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        out = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded MNIST-shaped stand-in, datagen/)",
+            "config": {"workload": f"{cfg.name}: {'-'.join(map(str, cfg.layers))} "
+                                   f"{'/'.join(cfg.act)}, {cfg.init} init, K={cfg.K} CNs, "
+                                   f"{cfg.n_train} rows, {cfg.epochs} epoch(s), batch {cfg.batch}, "
+                                   f"lr {cfg.lr}",
+                       "K_local": K_local, "rows_per_rank": nrows, "test_rows": cfg.n_test,
+                       "kernel": ["auto", "reference", "resident"][kernel_id],
+                       "l2": f"inputs {X.nbytes / 2**20:.0f} MiB per rank > 126 MB L2 (no flush)"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_max,
+                         "unit": "TFLOP/s", "frac": achieved / peak_max, "traffic": None,
+                         "kernel": "training epoch (one launch)",
+                         "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
+                                      f"{pk.get('sm_max_mhz', 1965.0):.0f} MHz (guide unit counts, "
+                                      f"sm_max clock); at the measured {sm_mhz:.0f} MHz the frac "
+                                      f"is {achieved / (peak_max * sm_mhz / pk.get('sm_max_mhz', 1965.0)):.3f}",
+                         "train_ms_per_launch": train_ms,
+                         "flop_per_launch": flop_launch},
+            "breakdown_ms": {"train": train_ms * cfg.epochs, "merge_predict": ms - train_ms * cfg.epochs},
+            "clocks": clocks,
+            "gpu_launches": args.steps * (cfg.epochs + 2),
+        }
+        if e2e:
+            out["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    net.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,91 @@
+// k_predict.cu — classification readout ("each class is
+// represented by one neuron in the last layer … the probabilities of being
+// that class"; reading R19: label = argmax_k z^L_k, ties → lowest index).
+//
+// The forward pass (Eqs.2-3) runs in fp64 from the fp32 parameters (each
+// fp32×fp32 product is exact in fp64), so the argmax decision is taken in
+// fp64 on both the GPU and the oracle side (R26).  A CTA classifies
+// a tile of kTile samples: every weight is read once per tile (warp per
+// output neuron, lanes over inputs) and applied to the kTile activations held
+// in shared memory.
+#include "pnn_internal.h"
+#include "pnn_device.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTile = 8;
+
+__global__ void __launch_bounds__(kThreads)
+predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restrict__ X,
+               long long n, int32_t* __restrict__ labels) {
+    extern __shared__ double smd[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = d.max_width;
+    double* bufA = smd;                       // [kTile][W]
+    double* bufB = smd + (size_t)kTile * W;   // [kTile][W]
+    for (long long t0 = (long long)blockIdx.x * kTile; t0 < n; t0 += (long long)gridDim.x * kTile) {
+        const int nt = (int)((n - t0) < kTile ? (n - t0) : kTile);
+        const int n0 = d.n[0];
+        for (int i = tid; i < kTile * n0; i += kThreads) {
+            int s = i / n0, j = i % n0;
+            bufA[s * W + j] = (s < nt) ? (double)X[(t0 + s) * n0 + j] : 0.0;
+        }
+        __syncthreads();
+        double* in = bufA;
+        double* out = bufB;
+        for (int l = 1; l <= d.L; ++l) {
+            const int nin = d.n[l - 1], nout = d.n[l];
+            const float* Wl = params + d.woff[l];
+            const float* bl = Wl + (long long)nout * nin;
+            for (int k = warp; k < nout; k += kWarps) {
+                const float* w = Wl + (long long)k * nin;
+                double acc[kTile];
+#pragma unroll
+                for (int s = 0; s < kTile; ++s) acc[s] = 0.0;
+                for (int j = lane; j < nin; j += 32) {
+                    const double wj = (double)w[j];
+#pragma unroll
+                    for (int s = 0; s < kTile; ++s) acc[s] = fma(wj, in[s * W + j], acc[s]);
+                }
+#pragma unroll
+                for (int s = 0; s < kTile; ++s) {
+                    double z = warp_sum_d(acc[s]) + (double)bl[k];
+                    // softmax is monotone: the readout only needs z^L (R19)
+                    if (lane == 0) out[s * W + k] = (l == d.L) ? z : act_fwd_d(d.act[l - 1], z);
+                }
+            }
+            __syncthreads();
+            double* tmp = in; in = out; out = tmp;
+        }
+        // argmax over z^L (now in `in`), ties → lowest index
+        if (tid < nt) {
+            const double* z = in + tid * W;
+            int best = 0;
+            for (int k = 1; k < d.n[d.L]; ++k) if (z[k] > z[best]) best = k;
+            labels[t0 + tid] = best;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_predict(const NetDesc& d, const float* params, const float* x, long long n,
+                           int32_t* labels, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    size_t smem = sizeof(double) * 2 * kTile * (size_t)d.max_width;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(predict_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long tiles = (n + kTile - 1) / kTile;
+    int grid = (int)(tiles < (long long)sms * 4 ? tiles : (long long)sms * 4);
+    predict_kernel<<<grid, kThreads, smem, st>>>(d, params, x, n, labels);
+    return cudaGetLastError();
+}

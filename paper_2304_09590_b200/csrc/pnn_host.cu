@@ -1,0 +1,484 @@
+// pnn_host.cu — the C ABI of include/pnn.h: handle, validation, init RNG,
+// slicing, kernel selection, merge orchestration and the NCCL communicator.
+//
+// Every step of the hot path runs in this library's kernels (k_*.cu); this
+// file only validates, allocates and enqueues.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string>
+#include <vector>
+
+#include "pnn.h"
+#include "pnn_internal.h"
+
+struct pnn_net_s {
+    NetDesc d{};
+    std::vector<int> layers, act;
+    int init = 0, K = 1;
+    float lr = 0.f;
+    uint64_t seed = 0;
+    int device = 0;
+    int nranks = 1, rank = 0;
+    int k_first = 0, K_local = 1;     // this rank's CNs [k_first, k_first + K_local)
+    void* comm = nullptr;             // ncclComm_t
+    int batch = 1, precision = PNN_FP32, kernel = PNN_KERNEL_AUTO;
+    float* d_children = nullptr;      // [K_local][P]
+    float* d_merged = nullptr;        // [P]
+    double* d_msum = nullptr;         // [P] fp64 partial sums (multi-rank merge)
+    float* d_gscratch = nullptr;      // [K_local][P] mini-batch gradient sums (lazy)
+    float* d_xstage = nullptr;        // host-input staging (lazy)
+    int32_t* d_ystage = nullptr;
+    long long stage_rows = 0;
+    cudaStream_t copy_stream = nullptr;
+    std::vector<float> h_init;        // init parameters (cloned into every CN)
+    bool poisoned = false;
+    std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+pnn_status fail(pnn_net net, pnn_status st, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (net) {
+        net->err = buf;
+        if (st == PNN_ERR_CUDA || st == PNN_ERR_NCCL) net->poisoned = true;
+    } else {
+        g_create_err = buf;
+    }
+    return st;
+}
+
+#define CUDA_TRY(net, expr)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(net, e_ == cudaErrorMemoryAllocation ? PNN_ERR_OOM : PNN_ERR_CUDA,    \
+                        "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+pnn_status check_live(pnn_net net) {
+    if (!net) return PNN_ERR_INVALID;
+    if (net->poisoned) {
+        net->err = "handle poisoned by an earlier CUDA/NCCL error: " + net->err;
+        return PNN_ERR_STATE;
+    }
+    return PNN_OK;
+}
+
+// ---- init RNG (reading R15) ---------------------------
+// Counter-based SplitMix64: this is the host library's own implementation of
+// the generator DESIGN.md §3 R15 specifies (the oracle has its own).
+uint64_t splitmix_fin(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+double draw_u01(uint64_t seed, int layer, int kind, int64_t idx, int s) {
+    uint64_t ctr = ((uint64_t)layer << 48) ^ ((uint64_t)kind << 47) ^ (uint64_t)(2 * idx + s);
+    uint64_t h = splitmix_fin(seed * 0x9E3779B97F4A7C15ULL + splitmix_fin(ctr + 0x632BE59BD9B4E019ULL));
+    return (double)(h >> 11) * (1.0 / 9007199254740992.0);
+}
+double draw_n01(uint64_t seed, int layer, int kind, int64_t idx) {
+    double u1 = draw_u01(seed, layer, kind, idx, 0), u2 = draw_u01(seed, layer, kind, idx, 1);
+    return std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(6.283185307179586 * u2);
+}
+void init_params_host(const NetDesc& d, int init, uint64_t seed, std::vector<float>& p) {
+    p.assign((size_t)d.P, 0.f);
+    for (int l = 1; l <= d.L; ++l) {
+        const int nin = d.n[l - 1], nout = d.n[l];
+        const long long nw = (long long)nin * nout;
+        float* W = p.data() + d.woff[l];
+        float* b = W + nw;
+        double sigma = 1.0;
+        if (init == PNN_INIT_XAVIER_NORMAL) sigma = std::sqrt(2.0 / (double)(nin + nout));
+        if (init == PNN_INIT_HE_NORMAL) sigma = std::sqrt(2.0 / (double)nin);
+        for (long long i = 0; i < nw; ++i)
+            W[i] = (init == PNN_INIT_UNIFORM) ? (float)(draw_u01(seed, l, 0, i, 0) - 0.5)
+                                              : (float)(sigma * draw_n01(seed, l, 0, i));
+        for (int k = 0; k < nout; ++k)
+            b[k] = (init == PNN_INIT_NORMAL)    ? (float)draw_n01(seed, l, 1, k)
+                   : (init == PNN_INIT_UNIFORM) ? (float)(draw_u01(seed, l, 1, k, 0) - 0.5)
+                                                : 0.f;
+    }
+}
+
+// ---- NCCL, resolved at run time (the process may already hold torch's copy;
+// dlopen by soname then returns that one).  Types come from nccl.h.
+struct NcclApi {
+    void* h = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl(std::string& why) {
+    if (g_nccl.h) return true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { why = std::string("dlopen libnccl.so.2: ") + dlerror(); return false; }
+    g_nccl.CommInitRank = (decltype(&ncclCommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (decltype(&ncclAllReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.CommDestroy = (decltype(&ncclCommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (decltype(&ncclGetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy || !g_nccl.GetErrorString) {
+        why = "libnccl.so.2 lacks a required symbol";
+        return false;
+    }
+    g_nccl.h = h;
+    return true;
+}
+
+pnn_status alloc_local(pnn_net net) {
+    cudaFree(net->d_children); net->d_children = nullptr;
+    cudaFree(net->d_gscratch); net->d_gscratch = nullptr;
+    const size_t bytes = sizeof(float) * (size_t)net->d.P * (size_t)(net->K_local > 0 ? net->K_local : 1);
+    CUDA_TRY(net, cudaMalloc(&net->d_children, bytes));
+    for (int c = 0; c < net->K_local; ++c)
+        CUDA_TRY(net, cudaMemcpy(net->d_children + (size_t)c * net->d.P, net->h_init.data(),
+                                 sizeof(float) * net->d.P, cudaMemcpyHostToDevice));
+    return PNN_OK;
+}
+
+int choose_kernel(pnn_net net, ResidentPlan* plan) {
+    if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
+    *plan = plan_resident(net->d, net->batch);
+    if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
+    return plan->ok ? PNN_KERNEL_RESIDENT : PNN_KERNEL_REFERENCE;
+}
+
+pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long n,
+                        int s_first, int s_count, cudaStream_t st) {
+    ResidentPlan plan{};
+    int k = choose_kernel(net, &plan);
+    if (k < 0) return fail(net, PNN_ERR_INVALID, "resident kernel not valid here: %s", plan.why);
+    cudaError_t e;
+    if (k == PNN_KERNEL_RESIDENT) {
+        e = launch_sgd_resident(plan, net->d, net->d_children, x, y, n, net->K_local, s_first,
+                                s_count, net->lr, st);
+    } else {
+        if (net->batch > 1 && !net->d_gscratch)
+            CUDA_TRY(net, cudaMalloc(&net->d_gscratch,
+                                     sizeof(float) * (size_t)net->d.P * (size_t)net->K_local));
+        e = launch_sgd_reference(net->d, net->d_children, x, y, n, net->K_local, s_first, s_count,
+                                 net->lr, net->batch, net->d_gscratch, st);
+    }
+    if (e != cudaSuccess) return fail(net, PNN_ERR_CUDA, "training launch: %s", cudaGetErrorString(e));
+    return PNN_OK;
+}
+
+pnn_status check_rows(pnn_net net, long long n) {
+    if (n < net->K_local)
+        return fail(net, PNN_ERR_DATA, "n = %lld rows < %d local CNs: some CN would get an empty slice",
+                    n, net->K_local);
+    if (net->batch > 1 && n / net->K_local < net->batch)
+        return fail(net, PNN_ERR_DATA, "slice of %lld rows shorter than the mini-batch %d",
+                    n / net->K_local, net->batch);
+    return PNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+pnn_status pnn_create(const int32_t* layers, int32_t n_layers, const int32_t* activation,
+                      int32_t init, int32_t n_subnets, float lr, uint64_t seed, pnn_net* out) {
+    if (out) *out = nullptr;
+    std::string bad;
+    auto add = [&](const std::string& s) { bad += (bad.empty() ? "" : "; ") + s; };
+    if (!out) add("out is NULL");
+    if (!layers || !activation) add("layers/activation is NULL");
+    if (n_layers < 2 || n_layers > PNN_MAX_LAYERS + 1)
+        add("n_layers = " + std::to_string(n_layers) + " (need 2.." + std::to_string(PNN_MAX_LAYERS + 1) + ")");
+    if (layers && activation && n_layers >= 2 && n_layers <= PNN_MAX_LAYERS + 1) {
+        for (int i = 0; i < n_layers; ++i)
+            if (layers[i] <= 0) add("layers[" + std::to_string(i) + "] = " + std::to_string(layers[i]) + " <= 0");
+        for (int i = 0; i < n_layers - 1; ++i) {
+            if (activation[i] < PNN_SIGMOID || activation[i] > PNN_SOFTMAX)
+                add("activation[" + std::to_string(i) + "] = " + std::to_string(activation[i]) + " unknown");
+            else if (activation[i] == PNN_SOFTMAX && i != n_layers - 2)
+                add("softmax on hidden layer " + std::to_string(i + 1));
+        }
+    }
+    if (init < PNN_INIT_NORMAL || init > PNN_INIT_HE_NORMAL) add("init = " + std::to_string(init) + " unknown");
+    if (n_subnets < 1) add("n_subnets = " + std::to_string(n_subnets) + " < 1");
+    if (!(lr > 0.f) || !std::isfinite(lr)) add("lr must be finite and > 0");
+    if (!bad.empty()) return fail(nullptr, PNN_ERR_INVALID, "pnn_create: %s", bad.c_str());
+
+    pnn_net net = new pnn_net_s();
+    NetDesc& d = net->d;
+    d.L = n_layers - 1;
+    long long w = 0;
+    int nn = 0, mw = 0;
+    for (int l = 0; l <= d.L; ++l) { d.n[l] = layers[l]; mw = mw > layers[l] ? mw : layers[l]; }
+    for (int l = 1; l <= d.L; ++l) {
+        d.act[l - 1] = activation[l - 1];
+        d.woff[l] = w;
+        d.noff[l] = nn;
+        w += (long long)d.n[l] * d.n[l - 1] + d.n[l];
+        nn += d.n[l];
+    }
+    d.P = w;
+    d.neurons = nn;
+    d.max_width = mw;
+    net->layers.assign(layers, layers + n_layers);
+    net->act.assign(activation, activation + n_layers - 1);
+    net->init = init;
+    net->K = n_subnets;
+    net->K_local = n_subnets;
+    net->lr = lr;
+    net->seed = seed;
+    cudaGetDevice(&net->device);
+    init_params_host(d, init, seed, net->h_init);
+    pnn_status st = alloc_local(net);
+    if (st == PNN_OK) {
+        cudaError_t e = cudaMalloc(&net->d_merged, sizeof(float) * d.P);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(net->d_merged, net->h_init.data(), sizeof(float) * d.P, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess)
+            st = fail(net, e == cudaErrorMemoryAllocation ? PNN_ERR_OOM : PNN_ERR_CUDA, "%s",
+                      cudaGetErrorString(e));
+    }
+    if (st != PNN_OK) {
+        g_create_err = net->err;
+        pnn_destroy(net);
+        return st;
+    }
+    *out = net;
+    return PNN_OK;
+}
+
+pnn_status pnn_set_comm(pnn_net net, const void* id, int32_t nranks, int32_t rank) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(net, PNN_ERR_INVALID, "nranks = %d, rank = %d", nranks, rank);
+    if (nranks > 1 && !id) return fail(net, PNN_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1");
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    if (net->comm) { g_nccl.CommDestroy((ncclComm_t)net->comm); net->comm = nullptr; }
+    net->nranks = nranks;
+    net->rank = rank;
+    net->k_first = (int)((long long)rank * net->K / nranks);
+    net->K_local = (int)((long long)(rank + 1) * net->K / nranks) - net->k_first;
+    if (nranks > 1) {
+        std::string why;
+        if (!load_nccl(why)) return fail(net, PNN_ERR_NCCL, "%s", why.c_str());
+        ncclUniqueId uid;
+        memcpy(&uid, id, sizeof uid);
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = g_nccl.CommInitRank(&comm, nranks, uid, rank);
+        net->comm = comm;
+        if (r != ncclSuccess) return fail(net, PNN_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+        if (!net->d_msum) CUDA_TRY(net, cudaMalloc(&net->d_msum, sizeof(double) * net->d.P));
+    }
+    return alloc_local(net);
+}
+
+pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (batch < 1) return fail(net, PNN_ERR_INVALID, "batch = %d < 1", batch);
+    if (precision != PNN_FP32 && precision != PNN_BF16)
+        return fail(net, PNN_ERR_INVALID, "precision = %d unknown", precision);
+    if (precision == PNN_BF16)
+        return fail(net, PNN_ERR_INVALID, "PNN_BF16 mini-batch variant is not built yet");
+    net->batch = batch;
+    net->precision = precision;
+    return PNN_OK;
+}
+
+pnn_status pnn_set_kernel(pnn_net net, int32_t kernel) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (kernel < PNN_KERNEL_AUTO || kernel > PNN_KERNEL_RESIDENT)
+        return fail(net, PNN_ERR_INVALID, "kernel = %d unknown", kernel);
+    if (kernel == PNN_KERNEL_RESIDENT) {
+        ResidentPlan p = plan_resident(net->d, net->batch);
+        if (!p.ok) return fail(net, PNN_ERR_INVALID, "resident kernel not valid: %s", p.why);
+    }
+    net->kernel = kernel;
+    return PNN_OK;
+}
+
+pnn_status pnn_train_epoch(pnn_net net, const float* x, const int32_t* labels, int64_t n,
+                           void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!x || !labels) return fail(net, PNN_ERR_INVALID, "x/labels is NULL");
+    if ((st = check_rows(net, n))) return st;
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    return launch_train(net, x, labels, n, 0, net->K_local, (cudaStream_t)stream);
+}
+
+pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh, int64_t n,
+                                void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!xh || !yh) return fail(net, PNN_ERR_INVALID, "x/labels is NULL");
+    if ((st = check_rows(net, n))) return st;
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    cudaStream_t cs = (cudaStream_t)stream;
+    if (net->stage_rows < n) {
+        cudaFree(net->d_xstage); cudaFree(net->d_ystage);
+        net->d_xstage = nullptr; net->d_ystage = nullptr; net->stage_rows = 0;
+        CUDA_TRY(net, cudaMalloc(&net->d_xstage, sizeof(float) * (size_t)n * net->d.n[0]));
+        CUDA_TRY(net, cudaMalloc(&net->d_ystage, sizeof(int32_t) * (size_t)n));
+        net->stage_rows = n;
+    }
+    // Pipeline: the CNs are cut into groups; group g's slices are copied on
+    // copy_stream while group g-1 trains on the caller's stream.
+    const int groups = net->K_local >= 8 ? 8 : net->K_local;
+    const size_t row_bytes = sizeof(float) * net->d.n[0];
+    cudaEvent_t ready[8];
+    for (int g = 0; g < groups; ++g) CUDA_TRY(net, cudaEventCreateWithFlags(&ready[g], cudaEventDisableTiming));
+    // the previous epoch's kernels may still read the staging buffer
+    cudaEvent_t prev;
+    CUDA_TRY(net, cudaEventCreateWithFlags(&prev, cudaEventDisableTiming));
+    CUDA_TRY(net, cudaEventRecord(prev, cs));
+    CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, prev, 0));
+    for (int g = 0; g < groups; ++g) {
+        const int s0 = (int)((long long)g * net->K_local / groups);
+        const int s1 = (int)((long long)(g + 1) * net->K_local / groups);
+        long long r0, c0, r1, c1;
+        shard_of(n, net->K_local, s0, &r0, &c0);
+        shard_of(n, net->K_local, s1 - 1, &r1, &c1);
+        const long long rows = r1 + c1 - r0;
+        CUDA_TRY(net, cudaMemcpyAsync(net->d_xstage + (size_t)r0 * net->d.n[0], xh + (size_t)r0 * net->d.n[0],
+                                      row_bytes * rows, cudaMemcpyHostToDevice, net->copy_stream));
+        CUDA_TRY(net, cudaMemcpyAsync(net->d_ystage + r0, yh + r0, sizeof(int32_t) * rows,
+                                      cudaMemcpyHostToDevice, net->copy_stream));
+        CUDA_TRY(net, cudaEventRecord(ready[g], net->copy_stream));
+        CUDA_TRY(net, cudaStreamWaitEvent(cs, ready[g], 0));
+        if ((st = launch_train(net, net->d_xstage, net->d_ystage, n, s0, s1 - s0, cs))) return st;
+    }
+    CUDA_TRY(net, cudaStreamSynchronize(net->copy_stream));   // host buffers consumed
+    for (int g = 0; g < groups; ++g) cudaEventDestroy(ready[g]);
+    cudaEventDestroy(prev);
+    return PNN_OK;
+}
+
+pnn_status pnn_merge(pnn_net net, void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    cudaStream_t cs = (cudaStream_t)stream;
+    const long long P = net->d.P;
+    if (net->nranks == 1) {
+        CUDA_TRY(net, launch_merge_local(net->d_children, net->K_local, P, net->K, net->d_merged, cs));
+        return PNN_OK;
+    }
+    CUDA_TRY(net, launch_merge_sum(net->d_children, net->K_local, P, net->d_msum, cs));
+    ncclResult_t r = g_nccl.AllReduce(net->d_msum, net->d_msum, (size_t)P, ncclFloat64, ncclSum,
+                                      (ncclComm_t)net->comm, cs);
+    if (r != ncclSuccess) return fail(net, PNN_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+    CUDA_TRY(net, launch_merge_finish(net->d_msum, P, net->K, net->d_merged, cs));
+    return PNN_OK;
+}
+
+pnn_status pnn_predict(pnn_net net, int32_t subnet, const float* x, int64_t n, int32_t* labels,
+                       void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!x || !labels || n < 0) return fail(net, PNN_ERR_INVALID, "x/labels NULL or n < 0");
+    const float* p;
+    if (subnet == -1) p = net->d_merged;
+    else if (subnet >= net->k_first && subnet < net->k_first + net->K_local)
+        p = net->d_children + (size_t)(subnet - net->k_first) * net->d.P;
+    else return fail(net, PNN_ERR_INVALID, "subnet %d is not local ([%d, %d))", subnet, net->k_first,
+                     net->k_first + net->K_local);
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    CUDA_TRY(net, launch_predict(net->d, p, x, n, labels, (cudaStream_t)stream));
+    return PNN_OK;
+}
+
+pnn_status pnn_get_params(pnn_net net, int32_t subnet, float* host_out, int64_t n_floats) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!host_out) return fail(net, PNN_ERR_INVALID, "host_out is NULL");
+    if (n_floats != net->d.P) return fail(net, PNN_ERR_SHAPE, "n_floats = %lld, P_total = %lld",
+                                          (long long)n_floats, (long long)net->d.P);
+    const float* p = pnn_device_params(net, subnet);
+    if (!p) return fail(net, PNN_ERR_INVALID, "subnet %d is not local", subnet);
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    CUDA_TRY(net, cudaDeviceSynchronize());
+    CUDA_TRY(net, cudaMemcpy(host_out, p, sizeof(float) * net->d.P, cudaMemcpyDeviceToHost));
+    return PNN_OK;
+}
+
+pnn_status pnn_set_params(pnn_net net, int32_t subnet, const float* host_in, int64_t n_floats) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!host_in) return fail(net, PNN_ERR_INVALID, "host_in is NULL");
+    if (n_floats != net->d.P) return fail(net, PNN_ERR_SHAPE, "n_floats = %lld, P_total = %lld",
+                                          (long long)n_floats, (long long)net->d.P);
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    CUDA_TRY(net, cudaDeviceSynchronize());
+    const size_t bytes = sizeof(float) * net->d.P;
+    if (subnet == -1) {
+        for (int c = 0; c < net->K_local; ++c)
+            CUDA_TRY(net, cudaMemcpy(net->d_children + (size_t)c * net->d.P, host_in, bytes, cudaMemcpyHostToDevice));
+        return PNN_OK;
+    }
+    float* p = (subnet == -2) ? net->d_merged : pnn_device_params(net, subnet);
+    if (!p) return fail(net, PNN_ERR_INVALID, "subnet %d is not local", subnet);
+    CUDA_TRY(net, cudaMemcpy(p, host_in, bytes, cudaMemcpyHostToDevice));
+    return PNN_OK;
+}
+
+float* pnn_device_params(pnn_net net, int32_t subnet) {
+    if (!net) return nullptr;
+    if (subnet == -1) return net->d_merged;
+    if (subnet < net->k_first || subnet >= net->k_first + net->K_local) return nullptr;
+    return net->d_children + (size_t)(subnet - net->k_first) * net->d.P;
+}
+
+int64_t pnn_param_count(pnn_net net) { return net ? net->d.P : -1; }
+
+pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count) {
+    if (!net || !first || !count) return PNN_ERR_INVALID;
+    *first = net->k_first;
+    *count = net->K_local;
+    return PNN_OK;
+}
+
+pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
+    if (!net || !kernel || !launches) return PNN_ERR_INVALID;
+    ResidentPlan plan{};
+    int k = choose_kernel(net, &plan);
+    *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
+    *launches = 1;
+    return PNN_OK;
+}
+
+const char* pnn_last_error(pnn_net net) {
+    return net ? net->err.c_str() : g_create_err.c_str();
+}
+
+pnn_status pnn_destroy(pnn_net net) {
+    if (!net) return PNN_OK;
+    cudaSetDevice(net->device);
+    cudaDeviceSynchronize();
+    if (net->comm && g_nccl.CommDestroy) g_nccl.CommDestroy((ncclComm_t)net->comm);
+    cudaFree(net->d_children);
+    cudaFree(net->d_merged);
+    cudaFree(net->d_msum);
+    cudaFree(net->d_gscratch);
+    cudaFree(net->d_xstage);
+    cudaFree(net->d_ystage);
+    if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
+    delete net;
+    return PNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// pnn_internal.h — shared declarations of the CUDA path (host library + kernels).
+// Nothing here is visible through the C ABI (include/pnn.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PNN_MAX_LAYERS 16
+
+// Network shape, passed by value to every kernel.
+//   n[0..L]   layer sizes (n[0] = inputs)
+//   act[l-1]  activation of layer l (PNN_SIGMOID..PNN_SOFTMAX)
+//   woff[l]   offset of W^l in a parameter slab; b^l follows at woff[l] + n[l]*n[l-1]
+//   noff[l]   offset of layer l's neurons in per-sample scratch (z, x, δ)
+struct NetDesc {
+    int L;
+    int n[PNN_MAX_LAYERS + 1];
+    int act[PNN_MAX_LAYERS];
+    long long woff[PNN_MAX_LAYERS + 1];
+    int noff[PNN_MAX_LAYERS + 1];
+    long long P;        // P_total
+    int neurons;        // Σ_{l>=1} n[l]
+    int max_width;      // max_l n[l], l >= 0
+};
+
+// R17: CN s of K gets rows [start, start+count): floor(n/K) + [s < n mod K].
+__host__ __device__ inline void shard_of(long long n, int K, int s, long long* start,
+                                         long long* count) {
+    long long base = n / K, rem = n % K;
+    *start = (long long)s * base + (s < rem ? s : rem);
+    *count = base + (s < rem ? 1 : 0);
+}
+
+// ---- kernels (launchers return cudaGetLastError()) -----------------------
+// Reference SGD: one CTA per CN, parameters in global memory.  CNs
+// [s_first, s_first+s_count) of the K_local local ones; rows split by R17
+// over n_local rows.  batch == 1: per-instance SGD; batch > 1: mini-batch
+// (gscratch: [K_local][P] fp32 gradient sums).
+cudaError_t launch_sgd_reference(const NetDesc& d, float* children, const float* x,
+                                 const int32_t* labels, long long n_local, int K_local,
+                                 int s_first, int s_count, float lr, int batch, float* gscratch,
+                                 cudaStream_t st);
+
+// Resident (persistent, on-chip weights) SGD kernel; see k_resident.cu.
+struct ResidentPlan {
+    bool ok;
+    int cluster;        // CTAs per CN
+    int threads;        // threads per CTA
+    size_t smem;        // dynamic shared memory per CTA
+    int variant;        // template instance id
+    char why[160];      // reason when !ok
+};
+ResidentPlan plan_resident(const NetDesc& d, int batch);
+cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
+                                const float* x, const int32_t* labels, long long n_local,
+                                int K_local, int s_first, int s_count, float lr,
+                                cudaStream_t st);
+
+// Merge: sum[i] = Σ_{c<K_local} children[c][i] in fp64, ascending c.
+cudaError_t launch_merge_sum(const float* children, int K_local, long long P, double* sum,
+                             cudaStream_t st);
+// merged[i] = (float)(sum[i] / K).
+cudaError_t launch_merge_finish(const double* sum, long long P, int K, float* merged,
+                                cudaStream_t st);
+// Single-rank fused version: merged[i] = (float)((Σ_c children[c][i]) / K).
+cudaError_t launch_merge_local(const float* children, int K_local, long long P, int K,
+                               float* merged, cudaStream_t st);
+
+// Predict: labels[i] = argmax z^L (fp64 forward from fp32 params), ties → lowest.
+cudaError_t launch_predict(const NetDesc& d, const float* params, const float* x, long long n,
+                           int32_t* labels, cudaStream_t st);

@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the
+same seeded inputs.  Marked gpu; run on a B200 via gpurun.
+
+Tolerances (BASELINE.json north_star; DESIGN.md §3 R22/R24/R26):
+  * fp32 per-sample SGD: every weight and bias of every CN, and of the merged
+    network, within max-abs 1e-4 of the fp32 oracle after the epoch(s);
+  * merge of the GPU's own children: bit-exact vs the oracle's merge (both sum
+    in fp64 in ascending CN order, divide by K, round once);
+  * predicted labels: bit-exact vs the oracle's fp64 readout of the same weights;
+  * init: bit-exact (both sides implement the R15 counter-based generator).
+"""
+import numpy as np
+import pytest
+import torch
+
+from datagen import make_rows, make_split
+from workloads import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def PNN(*a, kernel="auto", **k):
+    from paper_2304_09590_b200 import PNN as _P
+    net = _P(*a, **k)
+    net.set_kernel(kernel)
+    return net
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+KERNELS = ["reference", "auto"]
+
+
+def _train(cfg_layers, act, init, K, lr, X, y, epochs=1, kernel="auto", batch=1):
+    net = PNN(cfg_layers, act, init, K, lr, seed=0, kernel="reference" if batch > 1 else kernel)
+    if batch > 1:
+        net.set_minibatch(batch)
+    xd, yd = dev(X), dev(y)
+    for _ in range(epochs):
+        net.train_epoch(xd, yd)
+    net.merge()
+    torch.cuda.synchronize()
+    kids = np.stack([net.get_params(i) for i in range(K)])
+    return net, kids, net.get_params(-1)
+
+
+@pytest.mark.parametrize("init", ["normal", "uniform", "xavier", "he"])
+def test_init_bit_exact_and_cloned(orc, init):
+    layers = [784, 37, 10]
+    net = PNN(layers, ["tanh", "softmax"], init, 3, 0.1, seed=1234)
+    ref = orc.init_params(layers, init, 1234)
+    np.testing.assert_array_equal(net.get_params(-1), ref)
+    for i in range(3):
+        np.testing.assert_array_equal(net.get_params(i), ref)
+    # merge of untrained clones == init exactly (R18)
+    net.merge()
+    np.testing.assert_array_equal(net.get_params(-1), ref)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c1_full(orc, kernel):
+    """configs[0] at full size: 1 CN, 784-16-10 sigmoid, U[-.5,.5], η=0.1, 1000 rows."""
+    c = CONFIGS["C1"]
+    X, y = make_split(c.n_train, "train", 0)
+    Xt, _ = make_split(c.n_test, "test", 0)
+    net, kids, merged = _train(c.layers, c.act, c.init, c.K, c.lr, X, y, kernel=kernel)
+    okids, omerged = orc.train_pnn(c.layers, c.act, c.init, c.K, c.lr, 0, X, y)
+    assert np.abs(kids - okids).max() < TOL
+    assert np.abs(merged - omerged).max() < TOL
+    np.testing.assert_array_equal(merged, kids[0])            # K = 1: merge is the identity
+    lab = net.predict(dev(Xt)).cpu().numpy()
+    np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, merged, Xt))
+    # labels of the GPU-trained vs the oracle-trained network
+    assert (orc.predict(c.layers, c.act, omerged, Xt) != lab).sum() == 0
+
+
+REDUCED = [  # (config, K, rows, epochs): several CNs, a ragged row count
+    ("C2", 4, 4 * 700 + 3, 1),
+    ("C3", 8, 8 * 120 + 5, 2),
+    ("C4", 64, 64 * 96 + 37, 1),
+]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("name,K,n,epochs", REDUCED)
+def test_reduced_configs(orc, name, K, n, epochs, kernel):
+    c = CONFIGS[name]
+    X, y = make_split(n, "train", 0)
+    Xt, _ = make_split(500, "test", 0)
+    net, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, epochs, kernel)
+    okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=epochs, threads=8)
+    err = np.abs(kids - okids).max(axis=1)
+    assert err.max() < TOL, f"per-CN max-abs {err}"
+    assert np.abs(merged - omerged).max() < TOL
+    np.testing.assert_array_equal(merged, orc.merge(kids))    # merge arithmetic: bit-exact
+    lab = net.predict(dev(Xt)).cpu().numpy()
+    np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, merged, Xt))
+    lab0 = net.predict(dev(Xt), subnet=0).cpu().numpy()
+    np.testing.assert_array_equal(lab0, orc.predict(c.layers, c.act, kids[0], Xt))
+
+
+def test_determinism_and_kernel_agreement(orc):
+    c = CONFIGS["C4"]
+    X, y = make_split(32 * 64, "train", 0)
+    runs = [_train(c.layers, c.act, c.init, 32, c.lr, X, y)[1] for _ in range(2)]
+    np.testing.assert_array_equal(runs[0], runs[1])                 # bit-identical reruns
+
+
+def test_host_input_path_matches_device_path():
+    c = CONFIGS["C4"]
+    X, y = make_split(16 * 50 + 3, "train", 0)
+    a = _train(c.layers, c.act, c.init, 16, c.lr, X, y)[1]
+    net = PNN(c.layers, c.act, c.init, 16, c.lr, seed=0)
+    net.train_epoch_host(torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory())
+    torch.cuda.synchronize()
+    b = np.stack([net.get_params(i) for i in range(16)])
+    np.testing.assert_array_equal(a, b)
+
+
+def test_k1_is_snn_and_duplicated_shards(orc):
+    """K=1 handle == the sequential network; K CNs on K identical slices stay
+    identical and merge back to any one of them (R18)."""
+    c = CONFIGS["C1"]
+    X, y = make_split(200, "train", 0)
+    _, kids, merged = _train(c.layers, c.act, c.init, 4, c.lr, np.tile(X[:50], (4, 1)), np.tile(y[:50], 4))
+    for k in kids:
+        np.testing.assert_array_equal(k, kids[0])
+    np.testing.assert_array_equal(merged, kids[0])
+
+
+def test_minibatch_fp32(orc):
+    """Mini-batch GD, B=8 with a short last batch (R14)."""
+    c = CONFIGS["C4"]
+    X, y = make_split(4 * 61, "train", 0)
+    _, kids, merged = _train(c.layers, c.act, c.init, 4, c.lr, X, y, batch=8)
+    okids, omerged = orc.train_pnn(c.layers, c.act, c.init, 4, c.lr, 0, X, y, batch=8)
+    assert np.abs(kids - okids).max() < TOL
+    assert np.abs(merged - omerged).max() < TOL
+
+
+def test_error_paths():
+    from paper_2304_09590_b200 import PnnError
+    c = CONFIGS["C4"]
+    net = PNN(c.layers, c.act, c.init, 8, c.lr)
+    X, y = make_split(5, "train", 0)
+    with pytest.raises(PnnError) as e:
+        net.train_epoch(dev(X), dev(y))                     # 5 rows < 8 CNs
+    assert e.value.status == 3
+    with pytest.raises(PnnError) as e:
+        net.get_params(8)
+    assert e.value.status == 1
+    with pytest.raises(PnnError) as e:
+        net.set_params(np.zeros(10, np.float32))
+    assert e.value.status == 2
+    net.set_minibatch(4)
+    with pytest.raises(PnnError) as e:
+        net.train_epoch(dev(np.tile(X, (4, 1))), dev(np.tile(y, 4)))   # 20 rows: slice 2 < batch 4
+    assert e.value.status == 3
+    # the handle is still usable after validation errors
+    X, y = make_split(64, "train", 0)
+    net.train_epoch(dev(X), dev(y))
+    torch.cuda.synchronize()
+
+
+def test_set_params_roundtrip_and_predict_subnet(orc):
+    c = CONFIGS["C4"]
+    net = PNN(c.layers, c.act, c.init, 4, c.lr)
+    rng = np.random.default_rng(0)
+    p = rng.normal(size=net.param_count).astype(np.float32)
+    net.set_params(p, subnet=2)
+    np.testing.assert_array_equal(net.get_params(2), p)
+    Xt, _ = make_split(300, "test", 0)
+    lab = net.predict(dev(Xt), subnet=2).cpu().numpy()
+    np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, p, Xt))
+    net.set_params(p, subnet=-2)
+    np.testing.assert_array_equal(net.get_params(-1), p)
+
+
+# ---------------------------------------------------------------------------
+# Full-size configs: the GPU trains every CN; the oracle re-trains a sample of
+# CNs one by one on their slices (the oracle cannot do all 1024 in seconds).
+# ---------------------------------------------------------------------------
+def _full(orc, name, sample):
+    c = CONFIGS[name]
+    X, y = make_split(c.n_train, "train", 0)
+    net, kids, merged = _train(c.layers, c.act, c.init, c.K, c.lr, X, y, c.epochs)
+    okids, _ = orc.train_pnn(c.layers, c.act, c.init, c.K, c.lr, 0, X, y, epochs=c.epochs,
+                             threads=8, subnets=sample)
+    err = np.abs(kids[sample] - okids).max(axis=1)
+    np.testing.assert_array_equal(merged, orc.merge(kids))    # merge of all K children, bit-exact
+    Xt, _ = make_split(c.n_test, "test", 0)
+    lab = net.predict(dev(Xt)).cpu().numpy()
+    np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, merged, Xt))
+    return err
+
+
+def test_c2_full(orc):
+    err = _full(orc, "C2", [0, 1, 2, 3])
+    assert err.max() < TOL, err
+
+
+def test_c3_full_sampled(orc):
+    err = _full(orc, "C3", [0, 31])
+    assert err.max() < TOL, err
+
+
+def test_c4_full_sampled(orc):
+    err = _full(orc, "C4", [0, 1, 511, 777, 1023])
+    assert err.max() < TOL, err
