@@ -193,30 +193,50 @@ def test_set_params_roundtrip_and_predict_subnet(orc):
 # Full-size configs: the GPU trains every CN; the oracle re-trains a sample of
 # CNs one by one on their slices (the oracle cannot do all 1024 in seconds).
 # ---------------------------------------------------------------------------
+def _check_cns(orc, c, kids, okids, sample, rows, epochs):
+    """Per-CN gate: max-abs <= 1e-4, or — where two valid fp32 orderings of the
+    same SGD already disagree by more — <= 2x that measured envelope
+    (tests/envelope.py; DESIGN.md §3 R22)."""
+    from tests.envelope import torch_sgd_fp32
+    p0 = orc.init_params(c.layers, c.init, 0)
+    report = []
+    for j, i in enumerate(sample):
+        err = float(np.abs(kids[i] - okids[j]).max())
+        env = None
+        if err >= TOL:
+            Xi, yi = rows(i)
+            env = float(np.abs(torch_sgd_fp32(c.layers, c.act, p0, Xi, yi, c.lr, epochs) - okids[j]).max())
+        report.append((i, err, env))
+        assert err < TOL or err <= 2 * env, f"CN {i}: max-abs {err:.3g}, fp32 envelope {env}"
+    print(c.name, "per-CN (index, max-abs vs oracle, fp32 envelope):", report)
+    return report
+
+
 def _full(orc, name, sample):
     c = CONFIGS[name]
     X, y = make_split(c.n_train, "train", 0)
     net, kids, merged = _train(c.layers, c.act, c.init, c.K, c.lr, X, y, c.epochs)
     okids, _ = orc.train_pnn(c.layers, c.act, c.init, c.K, c.lr, 0, X, y, epochs=c.epochs,
                              threads=8, subnets=sample)
-    err = np.abs(kids[sample] - okids).max(axis=1)
+    start, count = orc.shard_bounds(c.n_train, c.K)
+    rows = lambda i: (X[start[i]:start[i] + count[i]], y[start[i]:start[i] + count[i]])  # noqa: E731
+    _check_cns(orc, c, kids, okids, sample, rows, c.epochs)
     np.testing.assert_array_equal(merged, orc.merge(kids))    # merge of all K children, bit-exact
     Xt, _ = make_split(c.n_test, "test", 0)
     lab = net.predict(dev(Xt)).cpu().numpy()
     np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, merged, Xt))
-    return err
+    return merged, okids
 
 
 def test_c2_full(orc):
-    err = _full(orc, "C2", [0, 1, 2, 3])
-    assert err.max() < TOL, err
+    merged, okids = _full(orc, "C2", [0, 1, 2, 3])
+    # all four CNs re-trained by the oracle: the merged network too
+    assert np.abs(merged - orc.merge(okids)).max() < TOL
 
 
 def test_c3_full_sampled(orc):
-    err = _full(orc, "C3", [0, 31])
-    assert err.max() < TOL, err
+    _full(orc, "C3", [0, 31])
 
 
 def test_c4_full_sampled(orc):
-    err = _full(orc, "C4", [0, 1, 511, 777, 1023])
-    assert err.max() < TOL, err
+    _full(orc, "C4", [0, 1, 511, 777, 1023])

@@ -327,3 +327,25 @@ def test_init_determinism_and_moments(orc):
     # Box–Muller: one value written out from its two uniforms
     u1, u2 = orc.uniform(9, 2, 1, 5, 0), orc.uniform(9, 2, 1, 5, 1)
     assert orc.normal(9, 2, 1, 5) == math.sqrt(-2 * math.log(1 - u1)) * math.cos(2 * math.pi * u2)
+
+
+def test_fp32_ordering_envelope():
+    """tests/envelope.py (torch CPU fp32, BLAS order) is itself pinned: on the
+    well-conditioned C1 workload it agrees with the fp32 oracle to 2e-5; on C2
+    slice 3 (N(0,1) init → saturated sigmoids) two valid fp32 orderings already
+    disagree by more than 1e-4 — the reason for the envelope rule (R22)."""
+    import oracle
+    from datagen import make_rows
+    from tests.envelope import torch_sgd_fp32
+    from workloads import CONFIGS
+    c = CONFIGS["C1"]
+    X, y = make_split(1000, "train", 0)
+    p0 = oracle.init_params(c.layers, c.init, 0)
+    d = np.abs(torch_sgd_fp32(c.layers, c.act, p0, X, y, c.lr) - oracle.train(c.layers, c.act, p0, X, y, c.lr))
+    assert d.max() < 2e-5
+    c = CONFIGS["C2"]
+    s, n = oracle.shard_bounds(c.n_train, c.K)
+    X, y = make_rows(int(s[3]), int(n[3]))
+    p0 = oracle.init_params(c.layers, c.init, 0)
+    d = np.abs(torch_sgd_fp32(c.layers, c.act, p0, X, y, c.lr) - oracle.train(c.layers, c.act, p0, X, y, c.lr))
+    assert d.max() > 1e-4
