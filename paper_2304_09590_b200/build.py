@@ -29,12 +29,15 @@ def _stale(out, deps):
     return not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), lib=None, objdir=None) -> str:
+    """Compile csrc/*.cu into `lib` (default libpnn.so).  `extra` nvcc flags
+    (e.g. -DPNN_SPIN_TAIL=1) build an experiment variant into its own lib/objdir."""
+    LIB_OUT = lib or LIB
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) \
         + [os.path.join(ROOT, "include", "pnn.h")]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = os.path.join(HERE, "build")
+    if not force and not _stale(LIB_OUT, deps):
+        return LIB_OUT
+    objdir = objdir or os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     hdrs = [d for d in deps if not d.endswith(".cu")]
     objs = []
@@ -43,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
-            cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+            cmd = [NVCC] + ARCH + FLAGS + list(extra) + ["-c", src, "-o", obj]
             procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for src, p in procs:
         out, _ = p.communicate()
@@ -54,11 +57,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(out.decode())
         with open(os.path.join(objdir, os.path.basename(src) + ".ptxas.txt"), "wb") as f:
             f.write(out)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = LIB_OUT + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, LIB_OUT)
+    return LIB_OUT
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--variant NAME -DFLAG=1 ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        i = args.index("--variant")
+        name = args[i + 1]
+        flags = [a for a in args[i + 2:] if a.startswith("-D")]
+        print(build(force=True, verbose="-v" in args, extra=flags,
+                    lib=os.path.join(HERE, f"libpnn_{name}.so"), objdir=os.path.join(HERE, f"build_{name}")))
+    else:
+        print(build(force="--force" in args, verbose="-v" in args))

@@ -66,3 +66,17 @@ __device__ __forceinline__ void softmax_warp(float* z, int n, int lane) {
     s = warp_sum(s);
     for (int k = lane; k < n; k += 32) z[k] = z[k] / s;
 }
+
+// Compile-time activation variants (no jump tables on the latency-critical tail).
+template <int A> __device__ __forceinline__ float act_fwd_t(float z) {
+    if constexpr (A == PNN_SIGMOID) return __frcp_rn(1.f + expf(-z));   // == 1.f/(1+e^-z), IEEE
+    else if constexpr (A == PNN_TANH) return tanhf(z);
+    else if constexpr (A == PNN_RELU) return z >= 0.f ? z : 0.f;
+    else return z;
+}
+template <int A> __device__ __forceinline__ float act_deriv_t(float x) {
+    if constexpr (A == PNN_SIGMOID) return x * (1.f - x);
+    else if constexpr (A == PNN_TANH) return 1.f - x * x;
+    else if constexpr (A == PNN_RELU) return x > 0.f ? 1.f : 0.f;
+    else return 1.f;
+}

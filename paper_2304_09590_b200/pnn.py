@@ -42,11 +42,13 @@ class PnnError(RuntimeError):
         self.status = status
 
 
-def load(path: str = LIB_PATH):
-    """Load libpnn.so and declare every signature of include/pnn.h."""
+def load(path: str | None = None):
+    """Load libpnn.so (or $PNN_LIB, an experiment variant) and declare every
+    signature of include/pnn.h."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PNN_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(there is no CPU fallback)")

@@ -1,4 +1,4 @@
-"""fp32 ordering envelope — test infrastructure for the parity tolerance.
+"""fp32 conditioning envelope — test infrastructure for the parity tolerance.
 
 Per-sample SGD is an iteration: after thousands of sequential updates, two
 correct fp32 implementations that merely sum in different orders drift apart,
@@ -7,8 +7,13 @@ and on ill-conditioned workloads (C2: N(0,1) init saturates the sigmoids, so
 north_star's 1e-4.  This module trains one CN with torch CPU fp32 (BLAS
 summation order, the paper's per-sample SGD written with torch ops) so a test
 can measure that spread: |torch_fp32 - oracle_fp32| is the disagreement of
-two valid fp32 orderings.  DESIGN.md §3 (R22) states the rule that uses it:
-a CN passes if max-abs(GPU - oracle_fp32) <= max(1e-4, 2 * envelope).
+two valid fp32 orderings.  A second measure needs no second implementation:
+re-run the fp32 oracle from the same init perturbed by 1 ulp per parameter
+(random direction) — how far the oracle itself moves is the precision to
+which fp32 arithmetic determines the result at all (perturbation_envelope).
+DESIGN.md §3 (R22) states the rule that uses them: a CN passes if
+max-abs(GPU - oracle_fp32) <= max(1e-4, 2 * envelope), envelope = the
+largest of the torch ordering and three 1-ulp perturbation runs.
 """
 import numpy as np
 import torch
@@ -52,3 +57,16 @@ def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1):
                 W[l] -= torch.outer(gl, xs[l])
                 b[l] -= gl
     return np.concatenate([np.concatenate([W[l].ravel().numpy(), b[l].numpy()]) for l in range(L)])
+
+
+def perturbation_envelope(orc, layers, act, params, X, y, lr, epochs=1, trials=3, seed=1):
+    """max over `trials` of max-abs(oracle(params ± 1 ulp) - oracle(params)), fp32."""
+    rng = np.random.default_rng(seed)
+    p0 = np.asarray(params, np.float32)
+    ref = orc.train(layers, act, p0, X, y, lr, epochs)
+    worst = 0.0
+    for _ in range(trials):
+        direction = np.where(rng.random(p0.size) < 0.5, np.inf, -np.inf).astype(np.float32)
+        pp = np.nextafter(p0, direction).astype(np.float32)
+        worst = max(worst, float(np.abs(orc.train(layers, act, pp, X, y, lr, epochs) - ref).max()))
+    return worst

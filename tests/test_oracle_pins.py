@@ -349,3 +349,11 @@ def test_fp32_ordering_envelope():
     p0 = oracle.init_params(c.layers, c.init, 0)
     d = np.abs(torch_sgd_fp32(c.layers, c.act, p0, X, y, c.lr) - oracle.train(c.layers, c.act, p0, X, y, c.lr))
     assert d.max() > 1e-4
+    # and the oracle itself moves by > 1e-4 under 1-ulp perturbations of the init (C2 slice 3),
+    # but by < 1e-5 on C1
+    from tests.envelope import perturbation_envelope
+    assert perturbation_envelope(oracle, c.layers, c.act, p0, X, y, c.lr, trials=1) > 1e-4
+    c1 = CONFIGS["C1"]
+    X1, y1 = make_split(1000, "train", 0)
+    assert perturbation_envelope(oracle, c1.layers, c1.act, oracle.init_params(c1.layers, c1.init, 0),
+                                 X1, y1, c1.lr, trials=1) < 1e-5
