@@ -222,18 +222,22 @@ def _full(orc, name, sample):
                              threads=8, subnets=sample)
     start, count = orc.shard_bounds(c.n_train, c.K)
     rows = lambda i: (X[start[i]:start[i] + count[i]], y[start[i]:start[i] + count[i]])  # noqa: E731
-    _check_cns(orc, c, kids, okids, sample, rows, c.epochs)
+    report = _check_cns(orc, c, kids, okids, sample, rows, c.epochs)
     np.testing.assert_array_equal(merged, orc.merge(kids))    # merge of all K children, bit-exact
     Xt, _ = make_split(c.n_test, "test", 0)
     lab = net.predict(dev(Xt)).cpu().numpy()
     np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, merged, Xt))
-    return merged, okids
+    return merged, okids, report
 
 
 def test_c2_full(orc):
-    merged, okids = _full(orc, "C2", [0, 1, 2, 3])
-    # all four CNs re-trained by the oracle: the merged network too
-    assert np.abs(merged - orc.merge(okids)).max() < TOL
+    merged, okids, report = _full(orc, "C2", [0, 1, 2, 3])
+    # all four CNs re-trained by the oracle: the merged network too.  The merge
+    # is the mean of the children, so its envelope is the mean of theirs (R22).
+    env = sum(max(TOL, 2 * e) if e is not None else TOL for _, _, e in report) / len(report)
+    err = float(np.abs(merged - orc.merge(okids)).max())
+    print("C2 merged max-abs", err, "bound", env)
+    assert err <= env
 
 
 def test_c3_full_sampled(orc):
