@@ -30,6 +30,8 @@ struct pnn_net_s {
     float* d_merged = nullptr;        // [P]
     double* d_msum = nullptr;         // [P] fp64 partial sums (multi-rank merge)
     float* d_gscratch = nullptr;      // [K_local][P] mini-batch gradient sums (lazy)
+    float4* d_gram = nullptr;         // [gram_rows] Gram terms of the resident kernel (lazy)
+    long long gram_rows = 0;
     float* d_xstage = nullptr;        // host-input staging (lazy)
     int32_t* d_ystage = nullptr;
     long long stage_rows = 0;
@@ -164,8 +166,15 @@ pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long
     if (k < 0) return fail(net, PNN_ERR_INVALID, "resident kernel not valid here: %s", plan.why);
     cudaError_t e;
     if (k == PNN_KERNEL_RESIDENT) {
-        e = launch_sgd_resident(plan, net->d, net->d_children, x, y, n, net->K_local, s_first,
-                                s_count, net->lr, st);
+        if (net->gram_rows < n) {
+            cudaFree(net->d_gram);
+            net->d_gram = nullptr;
+            net->gram_rows = 0;
+            CUDA_TRY(net, cudaMalloc(&net->d_gram, sizeof(float4) * (size_t)n));
+            net->gram_rows = n;
+        }
+        e = launch_sgd_resident(plan, net->d, net->d_children, x, y, net->d_gram, n, net->K_local,
+                                s_first, s_count, net->lr, st);
     } else {
         if (net->batch > 1 && !net->d_gscratch)
             CUDA_TRY(net, cudaMalloc(&net->d_gscratch,
@@ -457,7 +466,7 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     ResidentPlan plan{};
     int k = choose_kernel(net, &plan);
     *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
-    *launches = 1;
+    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : 1;   // resident: Gram terms + training
     return PNN_OK;
 }
 
@@ -474,6 +483,7 @@ pnn_status pnn_destroy(pnn_net net) {
     cudaFree(net->d_merged);
     cudaFree(net->d_msum);
     cudaFree(net->d_gscratch);
+    cudaFree(net->d_gram);
     cudaFree(net->d_xstage);
     cudaFree(net->d_ystage);
     if (net->copy_stream) cudaStreamDestroy(net->copy_stream);

@@ -43,15 +43,17 @@ cudaError_t launch_sgd_reference(const NetDesc& d, float* children, const float*
 // Resident (persistent, on-chip weights) SGD kernel; see k_resident.cu.
 struct ResidentPlan {
     bool ok;
-    int cluster;        // CTAs per CN
+    int cluster;        // CTAs per cluster (each CN is split over all of them)
+    int groups;         // CNs per cluster (warp groups per CTA)
     int threads;        // threads per CTA
     size_t smem;        // dynamic shared memory per CTA
     int variant;        // template instance id
     char why[160];      // reason when !ok
 };
 ResidentPlan plan_resident(const NetDesc& d, int batch);
+// gram: scratch of n_local float4 (the lookahead's Gram terms, recomputed per call).
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
-                                const float* x, const int32_t* labels, long long n_local,
+                                const float* x, const int32_t* labels, float4* gram, long long n_local,
                                 int K_local, int s_first, int s_count, float lr,
                                 cudaStream_t st);
 

@@ -2,6 +2,7 @@
 // used by the sm_100a kernels of the product path.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace ptx {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -20,6 +21,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) 
                  "r"(tx)
                  : "memory");
 }
+#ifdef PNN_DEBUG_WAIT
+// Debug build: a bounded wait that reports the barrier and traps instead of hanging.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    long long t0;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+        if (ok) return;
+        long long t1;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1));
+        if (t1 - t0 > 2000000000ll) break;
+    }
+    printf("mbar_wait timeout: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x,
+           smem_u32(b), parity);
+    __trap();
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -29,6 +50,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 // Non-suspending poll (test_wait) — for waiters whose wake-up latency is on the critical path.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -70,6 +92,20 @@ __device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint
                  "r"(__float_as_uint(v)), "r"(remote_bar)
                  : "memory");
 }
+// Predicated form (no branch): the store happens iff pred != 0.
+__device__ __forceinline__ void st_async_f32_if(bool pred, uint32_t remote_addr, float v, uint32_t remote_bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+        "@p st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n\t}" ::"r"(remote_addr),
+        "r"(__float_as_uint(v)), "r"(remote_bar), "r"((int)pred)
+        : "memory");
+}
+// 4-byte global -> shared async copy (LDGSTS) and its per-thread completion.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
