@@ -1,14 +1,11 @@
-// k_resident.cu — persistent per-sample SGD with register-resident weights (v7).
+// k_resident.cu — persistent per-sample SGD with register-resident weights (v8).
 //
-// A thread-block cluster of C CTAs trains NG child networks (CNs) over their
-// whole slices ("Each child-network learns only a slice").  Each
-// CN's hidden layer is split across the C SMs (CTA c owns units [c·U, c·U+U)),
-// and in every CTA the CN is served by NWG warps of 8 W¹ rows each; the rows
-// live in REGISTERS for the whole slice (loaded once, written back once).
-// C4 shape (784-128-10): C = 2, NG = 1, 8 warps per CTA; or C = 4, NG = 2,
-// 2 × 4 warps per CTA (every SM sub-partition then hosts one warp of each of
-// two independent CNs, so one CN's serial tail overlaps the other's sweep).
-// Scope: 2-layer nets D-H-O, 768 < D <= 784, O = 10, H <= 64·C/NG, per-sample SGD.
+// A thread-block cluster of C CTAs trains one child network (CN) over its whole
+// slice ("Each child-network learns only a slice").  The hidden
+// layer is split across the C SMs (C = 2 for the C4 shape 784-128-10): CTA c
+// owns units [c·U, c·U+U), U <= 64, served by 8 warps of 8 W¹ rows each; the
+// rows live in REGISTERS for the whole slice (loaded once, written back once).
+// Scope: 2-layer nets D-H-O, 768 < D <= 784, O = 10, H <= 64·C, per-sample SGD.
 //
 // Per sample, in the paper's sequential order (§3, Eqs.2-13):
 //   z1 = W1 x + b1, h = φ1(z1); z2 = W2 h + b2, x2 = φ2(z2)         (Eqs.2-5)
@@ -16,22 +13,28 @@
 //   δ1 = (W2ᵀ δ2) ⊙ φ1'(h), with the pre-update W2 (R6)              (Eq.11)
 //   W -= η δ xᵀ, b -= η δ                                             (Eqs.12-13)
 //
-// Two-step lookahead.  With W¹(t) the weights before sample t's update and
-// g(s) = η δ1(s), W¹(t) = W¹(t-2) - g(t-2)x(t-2)ᵀ - g(t-1)x(t-1)ᵀ, so
-//     z1(t) = W¹(t-2)x(t) - g(t-2)·G(t-2,t) - g(t-1)·G(t-1,t) + b1(t),
-// G(s,t) = x(s)·x(t): the paper's pre-activation in real arithmetic (DESIGN.md
-// R27; only the rounding differs).  The Gram terms depend on the data only;
-// gram_kernel computes them for every row before training and they travel
-// with x(t) through the shared-memory ring.  Step t of every warp:
-//   F(t)   acc = W¹(t-2)·x(t): lane l holds columns 4l+128q .. +3 (q < 6) as
-//          f32x2 pairs, one LDS.128 feeds 16 fma.rn.f32x2; columns 768..783
-//          live in shared memory (4 per lane); row sums by a transpose-reduce;
-//   U(t)   W¹ -= g(t-2)·x(t-2)ᵀ (g(t-2) is two steps old: no wait);
-//   tail   wait for the partial logits of sample t-1 from every warp of the
-//          cluster (mbarrier zfull, st.async from the peers); z2, softmax /
-//          φ2 and δ2(t-1) in every lane; δ1 and g(t-1) of the warp's units,
-//          their W² columns, b1, b2; then z1(t) by the correction above, h(t)
-//          and the partial logits of the warp's units, published to every CTA.
+// L-step lookahead (L = 4).  With W¹(t) the weights before sample t's update
+// and g(s) = η δ1(s), W¹(t) = W¹(t-L) - Σ_{s=t-L}^{t-1} g(s) x(s)ᵀ, so
+//     z1(t) = W¹(t-L) x(t) - Σ_{k=1..L} g(t-k)·G(t-k,t) + b1(t),  G(s,t) = x(s)·x(t),
+// the paper's pre-activation in real arithmetic (R27; only the
+// rounding differs).  The Gram terms depend on the data only: gram_kernel
+// computes them (and stages the label) for every row before training, and they
+// travel with x(t) through the shared-memory ring.
+//
+// Warp roles.  Every warp sweeps its rows each step s:
+//   F(s)  acc = W¹(s-L)·x(s) (lane l: columns 4l+128q .. +3, q < 6, as f32x2
+//         pairs, one LDS.128 feeds 16 fma.rn.f32x2; columns 768..783 in shared
+//         memory), row sums → shared memory, arrive aready(s);
+//   U(s)  wait gready(s-L), W¹ -= g(s-L)·x(s-L)ᵀ.
+// The serial per-sample chain runs on ONE warp per CTA at a time: sample c's
+// chain is done by warp c mod 8 (after its own F(c+1)), for all of the CTA's
+// units, with W², b1, b2 and the g history in shared memory: z1(c) by the
+// correction above, h(c), the CTA's partial logits (published to every CTA of
+// the cluster through st.async + mbarrier zfull), then z2, softmax / φ2 and
+// δ2(c) in every lane, δ1, g(c), the W²/b1/b2 updates, arrive gready(c).  The
+// other warps never wait for the chain except through gready(s-L), L samples
+// later, so the sweeps run at their own pace while the chain's latency (the
+// cross-SM exchange above all) overlaps them.
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -47,32 +50,37 @@ namespace {
 using namespace ptx;
 
 constexpr int R = 8;          // W1 rows per warp
+constexpr int NW = 8;         // warps per CTA
+constexpr int UMAX = R * NW;  // units per CTA
 constexpr int NQ = 6;         // column quads per lane: columns [0, 768)
 constexpr int NP = 2 * NQ;    // f32x2 pairs per lane
 constexpr int XC = 768;       // first shared-memory column
-constexpr int GOFF = 784;     // Gram terms of sample u sit at its x ring slot + GOFF
+constexpr int GOFF = 784;     // gram record of sample u sits at its x ring slot + GOFF
 constexpr int DP = 800;       // x ring slot stride (floats)
-constexpr int S = 12;         // x ring slots per CN group
-constexpr int PF = S - 3;     // prefetch distance
+constexpr int LAG = 4;        // lookahead L
+constexpr int S = 16;         // x ring slots
+constexpr int PF = 8;         // prefetch distance (<= S - 1 - LAG)
 constexpr int O = 10;         // outputs
+constexpr int AR = 8;         // row-sum ring slots (> LAG + 1)
+constexpr int GR = 8;         // g ring slots (> LAG)
+static_assert(AR > LAG + 1 && GR > LAG, "ring sizes");
 constexpr int ZS = 4;         // partial-logit ring slots
 constexpr int CMAX = 4;       // cluster size
-constexpr int NWMAX = 8;      // warps per CTA
-constexpr int NGMAX = 2;      // CN groups per CTA
 constexpr int kTraceT = 64, kTraceP = 8;   // debug timeline: [cta][warp][t][point]
 
-struct __align__(16) GroupSmem {
-    uint64_t xfull[S];                    // x(u) and its Gram terms landed
-    uint64_t zfull[ZS];                   // partial logits of sample t from every warp of the CN
-    float zbuf[ZS][CMAX * NWMAX][16];     // [t % ZS][cta·NWG + warp][o]
-    float gw[2][NWMAX][R];                // [s & 1][warp][row] g(s) of the warp's rows
-};
 struct __align__(16) Smem {
-    GroupSmem grp[NGMAX];
-    float wx[NWMAX][R][16];               // W1 columns 768..783 of each warp's rows
-    float zg[NWMAX][16];                  // per-warp all-gather of z2
-    float b2s[NWMAX][16];                 // per-warp copy of b2 (identical in every warp)
-    int32_t ylab[NWMAX][64];              // per-warp label ring: [warp][u & 63] = y(u)
+    uint64_t xfull[S];                 // x(u) and its gram record landed
+    uint64_t aready[AR];               // all warps' row sums of sample s (count NW)
+    uint64_t gready[GR];               // chain → sweeps: g(c) of every row (the pair: count 2)
+    uint64_t zfull[ZS];                // partial logits of sample c from every CTA (count 2 + tx)
+    float asum[AR][UMAX][4];           // [s % AR][row][part] partial row sums of acc(s)
+    float gbuf[GR][UMAX];              // [c % GR][row] g(c)
+    float zbuf[ZS][2 * CMAX][16];      // [c % ZS][2·cta + half][o] partial logits
+    float w2s[UMAX][16];               // W2[o][k0 + u] (o < 10), the CTA's units
+    float b1s[UMAX];                   // b1 of the CTA's units
+    float b2s[2][16];                  // b2 before sample c at [c & 1] (identical in every CTA)
+    float hs[2][UMAX];                 // h(c) of the CTA's units, [c & 1]
+    float wx[NW][R][16];               // W1 columns 768..783 of each warp's rows
 };
 constexpr size_t kSmemHead = ((sizeof(Smem) + 127) / 128) * 128;
 
@@ -102,18 +110,14 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
     asm volatile("mov.b64 %0, %0;" : "+l"(p));
     return p;
 }
-// v[base + q] for a lane-dependent q in 0..3, without local memory
-__device__ __forceinline__ float pick4(const float* v, int base, int q) {
-    const float a = v[base], b = v[base + 1], c = v[base + 2], d = v[base + 3];
-    return q == 0 ? a : q == 1 ? b : q == 2 ? c : d;
-}
 
-// Gram terms of every row of CNs [s_first, s_first + s_count) (shard-local index u):
-// gram[row] = {x(u-2)·x(u), x(u-1)·x(u), 0, 0}, terms before the slice start = 0.
-// One warp per row; X is read once from HBM (the two previous rows hit in cache).
+// Gram record of every row of CNs [s_first, s_first + s_count) (shard-local index u):
+// rec[2·row] = {x(u-4)·x(u), x(u-3)·x(u), x(u-2)·x(u), x(u-1)·x(u)} (0 before the slice
+// start), rec[2·row + 1] = {label bits, 0, 0, 0}.  One warp per row; X is read once from
+// HBM (the four previous rows hit in cache).
 __global__ void __launch_bounds__(256)
-gram_kernel(const float* __restrict__ X, int D, long long n_local, int K_local, int s_first,
-            int s_count, float4* __restrict__ gram) {
+gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, long long n_local,
+            int K_local, int s_first, int s_count, float4* __restrict__ rec) {
     long long r0, c0, r1, c1;
     shard_of(n_local, K_local, s_first, &r0, &c0);
     shard_of(n_local, K_local, s_first + s_count - 1, &r1, &c1);
@@ -130,112 +134,110 @@ gram_kernel(const float* __restrict__ X, int D, long long n_local, int K_local, 
         shard_of(n_local, K_local, (int)s, &st, &cnt);
         const long long u = row - st;
         const float* xc = X + row * (long long)D;
-        float g0 = 0.f, g1 = 0.f;
+        float gk[4] = {0.f, 0.f, 0.f, 0.f};        // gk[4-k] = x(u-k)·x(u)
         for (int j = lane * 4; j < D; j += 128) {
             const float4 c = *reinterpret_cast<const float4*>(xc + j);
-            if (u >= 1) {
-                const float4 b = *reinterpret_cast<const float4*>(xc - D + j);
-                g1 = fmaf(b.w, c.w, fmaf(b.z, c.z, fmaf(b.y, c.y, fmaf(b.x, c.x, g1))));
-            }
-            if (u >= 2) {
-                const float4 a = *reinterpret_cast<const float4*>(xc - 2 * D + j);
-                g0 = fmaf(a.w, c.w, fmaf(a.z, c.z, fmaf(a.y, c.y, fmaf(a.x, c.x, g0))));
+#pragma unroll
+            for (int k = 1; k <= 4; ++k) {
+                if (u >= k) {
+                    const float4 b = *reinterpret_cast<const float4*>(xc - k * D + j);
+                    gk[4 - k] = fmaf(b.w, c.w, fmaf(b.z, c.z, fmaf(b.y, c.y, fmaf(b.x, c.x, gk[4 - k]))));
+                }
             }
         }
-        g0 = warp_sum(g0);
-        g1 = warp_sum(g1);
-        if (lane == 0) gram[row] = make_float4(g0, g1, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gk[k] = warp_sum(gk[k]);
+        if (lane == 0) {
+            rec[2 * row] = make_float4(gk[0], gk[1], gk[2], gk[3]);
+            rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), 0.f, 0.f, 0.f);
+        }
     }
 }
 
-template <int C, int NG, int A1, int A2, bool TRACE>
-__global__ void __launch_bounds__(NWMAX * 32, 1)
+template <int C, int A1, int A2, bool TRACE>
+__global__ void __launch_bounds__(NW * 32, 1)
 sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ X,
-                    const int32_t* __restrict__ Y, const float4* __restrict__ gram, long long n_local,
-                    int K_local, int s_first, int s_count, float lr, long long* __restrict__ trace) {
+                    const float4* __restrict__ rec, long long n_local, int K_local, int s_first,
+                    float lr, long long* __restrict__ trace) {
     extern __shared__ __align__(128) unsigned char smraw[];
     Smem& sm = *reinterpret_cast<Smem*>(smraw);
+    float* xring = reinterpret_cast<float*>(smraw + kSmemHead);
     const int D = d.n[0], H = d.n[1];
-    constexpr int NWG = NWMAX / NG;                // warps per CN group
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = warp / NWG, wl = warp % NWG;     // CN group, warp within the group
-    GroupSmem& gs = sm.grp[g];
-    float* xring = reinterpret_cast<float*>(smraw + kSmemHead) + g * (S + 1) * DP;
     const int crank = (C > 1) ? (int)cluster_rank() : 0;
-    const int cidx = s_first + (int)(blockIdx.x / C) * NG + g;   // this group's CN
-    const bool active = cidx < s_first + s_count;
+    const int cn = s_first + (int)(blockIdx.x / C);
     const int U = (H + C - 1) / C;                 // units per CTA
     const int k0 = crank * U;
     const int Uown = max(0, min(U, H - k0));
 
-    long long row0 = 0, T64 = 0;
-    if (active) shard_of(n_local, K_local, cidx, &row0, &T64);
+    long long row0, T64;
+    shard_of(n_local, K_local, cn, &row0, &T64);
     const int T = (int)T64;
-    float* P = children + (long long)(active ? cidx : s_first) * d.P;
+    float* P = children + (long long)cn * d.P;
     float* W1 = P;
     float* b1g = P + (long long)H * D;
     float* W2 = b1g + H;
     float* b2g = W2 + (long long)O * H;
     const float* Xc = X + row0 * (long long)D;
-    const int32_t* Yc = Y + row0;
-    const float4* Gc = gram + row0;
+    const float4* Rc = rec + 2 * row0;
+    const uint32_t xbytes = (uint32_t)D * 4u;
 
     if (threadIdx.x == 0) {
-        for (int q = 0; q < NG; ++q) {
-            for (int i = 0; i < S; ++i) mbar_init(&sm.grp[q].xfull[i], 1);
-            for (int i = 0; i < ZS; ++i) mbar_init(&sm.grp[q].zfull[i], NWG);
-        }
+        for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
+        for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NW);
+        for (int i = 0; i < GR; ++i) mbar_init(&sm.gready[i], 2);
+        for (int i = 0; i < ZS; ++i) mbar_init(&sm.zfull[i], 2);
         fence_mbar_init();
     }
-    {
-        float* ring0 = reinterpret_cast<float*>(smraw + kSmemHead);
-        for (int i = threadIdx.x; i < NG * (S + 1) * DP; i += blockDim.x) ring0[i] = 0.f;
-        for (int q = 0; q < NG; ++q)
-            for (int i = threadIdx.x; i < 2 * NWMAX * R; i += blockDim.x) (&sm.grp[q].gw[0][0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < (S + 1) * DP; i += blockDim.x) xring[i] = 0.f;   // + zero row
+    for (int i = threadIdx.x; i < GR * UMAX; i += blockDim.x) (&sm.gbuf[0][0])[i] = 0.f;
+
+    for (int i = threadIdx.x; i < UMAX * 16; i += blockDim.x) {
+        const int u = i >> 4, o = i & 15;
+        sm.w2s[u][o] = (u < Uown && o < O) ? W2[(long long)o * H + k0 + u] : 0.f;
     }
+    for (int i = threadIdx.x; i < UMAX; i += blockDim.x) sm.b1s[i] = (i < Uown) ? b1g[k0 + i] : 0.f;
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) (&sm.b2s[0][0])[i] = (i < O) ? b2g[i] : 0.f;
     fence_proxy_async_smem();
     __syncthreads();
     if constexpr (C > 1) cluster_sync_all();       // peers' barriers exist before any st.async
-    const uint32_t xbytes = (uint32_t)D * 4u;
-    if (active && wl == 0 && lane == 0)
-        for (int u = 0; u <= PF && u < T; ++u) {   // steps t >= 1 issue x(t + PF)
-            uint64_t* bar = &gs.xfull[u];
-            mbar_arrive_expect_tx(bar, xbytes + 16u);
-            bulk_g2s(xring + u * DP, Xc + (long long)u * D, xbytes, bar);
-            bulk_g2s(xring + u * DP + GOFF, Gc + u, 16u, bar);
-        }
+    auto issue_x = [&](int u, int slot) {
+        uint64_t* bar = &sm.xfull[slot];
+        mbar_arrive_expect_tx(bar, xbytes + 32u);
+        bulk_g2s(xring + slot * DP, Xc + (long long)u * D, xbytes, bar);
+        bulk_g2s(xring + slot * DP + GOFF, Rc + 2 * u, 32u, bar);
+    };
+    if (threadIdx.x == 0)
+        for (int u = 0; u < PF && u < T; ++u) issue_x(u, u);   // the chain of sample c issues x(c+PF)
 
 #define TR(pt)                                                                                   \
     do {                                                                                         \
         if constexpr (TRACE) {                                                                   \
-            if (blockIdx.x < 2 && t < kTraceT && lane == 0)                                      \
-                trace[(((int)blockIdx.x * NWMAX + warp) * kTraceT + t) * kTraceP + (pt)] =       \
+            if (blockIdx.x < 2 && s < kTraceT && lane == 0)                                      \
+                trace[(((int)blockIdx.x * NW + warp) * kTraceT + s) * kTraceP + (pt)] =          \
                     ptx::clock64();                                                              \
         }                                                                                        \
     } while (0)
 
     // ---- this warp's W1 rows ----
-    const int kr0 = wl * R;                        // first row (CTA-local)
+    const int kr0 = warp * R;                      // first row (CTA-local)
     uint64_t w[R][NP];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const bool live = active && kr0 + r < Uown;
+        const bool live = kr0 + r < Uown;
         const float* src = W1 + (long long)(k0 + kr0 + r) * D;
 #pragma unroll
         for (int m = 0; m < NP; ++m)
             w[r][m] = live ? *reinterpret_cast<const uint64_t*>(src + pcol(lane, m)) : 0ull;
     }
-    // ---- tail state: lane = 4·r + q holds unit r: W2[o][·] for o = q, q+4, q+8 and the
-    //      W1 columns 768+4q .. 768+4q+3 (in shared memory) ----
-    const int tr = lane >> 2, tq = lane & 3;
-    const bool tlive = active && kr0 + tr < Uown;
-    const int ku = k0 + kr0 + tr;                  // global hidden unit of this lane
-    const int nx = D - XC - 4 * tq;                // valid extra columns of this lane's quad
+    const int tr = lane >> 2, tq = lane & 3;       // columns 768+4tq .. +3 of row tr
+    const int nx = D - XC - 4 * tq;
+    const bool xlive = kr0 + tr < Uown;
     float* wxp = &sm.wx[warp][tr][4 * tq];
     {
         float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float* src = W1 + (long long)ku * D + XC + 4 * tq;
-        if (tlive) {
+        const float* src = W1 + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
+        if (xlive) {
             if (nx > 0) w4.x = src[0];
             if (nx > 1) w4.y = src[1];
             if (nx > 2) w4.z = src[2];
@@ -243,42 +245,30 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         }
         *reinterpret_cast<float4*>(wxp) = w4;
     }
-    float w2[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const int o = tq + 4 * i;
-        w2[i] = (tlive && o < O) ? W2[(long long)o * H + ku] : 0.f;
-    }
-    float b1 = tlive ? b1g[ku] : 0.f;
-    if (lane < 16) sm.b2s[warp][lane] = (active && lane < O) ? b2g[lane] : 0.f;
-    float hprev = 0.f, gm1 = 0.f, gm2 = 0.f;       // h(t-1), g(t-1), g(t-2) of this lane's unit
-    if (lane < T) cp_async4(&sm.ylab[warp][lane], Yc + lane);
-    if (32 + lane < T) cp_async4(&sm.ylab[warp][32 + lane], Yc + 32 + lane);
-    cp_async_commit();
-    cp_async_wait_all();
     __syncwarp();
 
-    // DSMEM address of zbuf[0][crank·NWG + wl][0] in each peer (its zfull[0] is at a fixed offset)
-    uint32_t rz[C > 1 ? C - 1 : 1];
+    // chain side: the pair of warps (2p, 2p+1) runs the chain of samples c ≡ p (mod 4); warp
+    // 2p+h owns units 32h + lane (h = warp & 1), the two warps sit on different SM sub-partitions
+    const int half = warp & 1;
+    const int uc = 32 * half + lane;               // this lane's unit in the chain
+    const bool lc = uc < Uown;
+    const int zrow = 2 * crank + half;             // this warp's row of zbuf in every CTA
+    uint32_t rz[C > 1 ? C - 1 : 1];                // DSMEM address of zbuf[0][zrow][0] in each peer
     if constexpr (C > 1) {
 #pragma unroll
         for (int p = 1; p < C; ++p)
-            rz[p - 1] = mapa(smem_u32(&gs.zbuf[0][crank * NWG + wl][0]), (uint32_t)((crank + p) % C));
+            rz[p - 1] = mapa(smem_u32(&sm.zbuf[0][zrow][0]), (uint32_t)((crank + p) % C));
     }
-    constexpr uint32_t kZStride = CMAX * NWMAX * 16 * 4;
-    constexpr uint32_t kZfullOff = (uint32_t)offsetof(GroupSmem, zfull) - (uint32_t)offsetof(GroupSmem, zbuf);
+    constexpr uint32_t kZStride = 2 * CMAX * 16 * 4;
+    constexpr uint32_t kZfullOff = (uint32_t)offsetof(Smem, zfull) - (uint32_t)offsetof(Smem, zbuf);
 
-    float a = 0.f;                                 // acc(t) of row tr (after the reduction)
-    int sx = 0;                                    // ring slot of x(t) = t % S
-    uint32_t xpar = 0;                             // phase parity of x(t)'s slot = (t / S) & 1
-    int sz = 0, pz = ZS - 1;                       // zbuf slots of samples t and t-1
-    uint32_t zpar = 0, ppar = 1;                   // phase parities of zfull(t), zfull(t-1)
-    for (int t = 0; active && t <= T + 1; ++t) {
+    int sx = 0;                                    // ring slot of x(s) = s % S
+    for (int s = 0; s <= T + LAG; ++s) {
         TR(0);
-        if (t < T) {
-            // x(t) is certified by zfull(t-2) (waited in step t-1); the first two wait here
-            if (t <= 1) mbar_wait(&gs.xfull[t], 0u);
-            // ---------------- F(t): acc = W¹(t-2)·x(t) ----------------
+        if (s < T) {
+            // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
+            if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
+            // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
             const float* xn = xring + sx * DP + 4 * lane;
             uint64_t acc[R];
 #pragma unroll
@@ -310,7 +300,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 upk(acc[r], lo, hi);
                 v[r] = lo + hi;
             }
-            // transpose-reduce 8 row sums over 32 lanes; row (lane >> 2) ends in its 4 lanes
+            // transpose-reduce 8 row sums over lanes 16/8/4: row (lane >> 2), part (lane & 3)
             const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
             float u4[4];
 #pragma unroll
@@ -320,16 +310,19 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 #pragma unroll
             for (int i = 0; i < 2; ++i)
                 u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
-            a = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
-            a += __shfl_xor_sync(0xffffffffu, a, 2);
-            a += __shfl_xor_sync(0xffffffffu, a, 1);
+            const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
+            sm.asum[s % AR][kr0 + tr][tq] = part;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
         }
         TR(1);
-        if (t >= 2) {
-            // ---------------- U(t): W¹ -= g(t-2)·x(t-2)ᵀ ----------------
-            const int s2 = (sx >= 2) ? sx - 2 : sx + S - 2;
-            const float* xo = xring + s2 * DP + 4 * lane;
-            const float4* gv = reinterpret_cast<const float4*>(&gs.gw[t & 1][wl][0]);
+        if (s >= LAG && s - LAG < T) {
+            // ---------------- U(s): W¹ -= g(s-L)·x(s-L)ᵀ ----------------
+            const int u = s - LAG;
+            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+            const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
+            const float* xo = xring + su * DP + 4 * lane;
+            const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
             const float4 g0 = gv[0], g1 = gv[1];
             const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
             uint64_t xa, xb;
@@ -347,171 +340,206 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 xb = nb;
             }
             float4 w4 = *reinterpret_cast<const float4*>(wxp);
-            const float4 x4 = *reinterpret_cast<const float4*>(xring + s2 * DP + XC + 4 * tq);
-            const float gq = -gs.gw[t & 1][wl][tr];
+            const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
+            const float gq = -sm.gbuf[u % GR][kr0 + tr];
             w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
             w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
             *reinterpret_cast<float4*>(wxp) = w4;
         }
         TR(2);
-        if (t > T) break;
 
-        // ================= tail: finish sample t-1, start sample t =================
-        if (t >= 33 && ((t - 1) & 31) == 0) {      // refill the half of the label ring used 32 ago
-            if (t + 31 + lane < T) cp_async4(&sm.ylab[warp][(t + 31 + lane) & 63], Yc + t + 31 + lane);
-            cp_async_commit();
-        }
-        if (t >= 49 && ((t - 1) & 31) == 16) {
-            cp_async_wait_all();
-            __syncwarp();
-        }
-        // δ2(t-1)[o] in lanes o and o+16 (o < 10; δ2(-1) := 0), lane-parallel softmax
-        float dl = 0.f;
-        if (t >= 1) {
-            mbar_wait(&gs.zfull[pz], ppar);
+        // ================= the chain of sample c = s - 1 (a pair of warps per sample) =================
+        const int c = s - 1;
+        if (c >= 0 && c < T && (c & 3) == (warp >> 1)) {
+            const int cs = (sx >= 1) ? sx - 1 : S - 1;          // ring slot of x(c)
+            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));   // every warp's row sums of c
+            if (c >= 1) mbar_wait(&sm.gready[(c - 1) % GR], (uint32_t)(((c - 1) / GR) & 1));   // chain c-1
             TR(3);
-            // every local warp has passed step t-1: the slot of x(t-3) is free for x(t+PF)
-            if (wl == 0 && lane == 0 && t + PF < T) {
-                const int u = t + PF, su = (sx + PF >= S) ? sx + PF - S : sx + PF;
-                uint64_t* bar = &gs.xfull[su];
-                mbar_arrive_expect_tx(bar, xbytes + 16u);
-                bulk_g2s(xring + su * DP, Xc + (long long)u * D, xbytes, bar);
-                bulk_g2s(xring + su * DP + GOFF, Gc + u, 16u, bar);
+            // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c); h(c) of unit uc ----
+            const float4 G = *reinterpret_cast<const float4*>(xring + cs * DP + GOFF);
+            const int label = __float_as_int(xring[cs * DP + GOFF + 4]);
+            const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][uc][0]);
+            float z = (pa.x + pa.y) + (pa.z + pa.w);
+            z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);
+            z = fmaf(-sm.gbuf[(c + GR - 3) % GR][uc], G.y, z);
+            z = fmaf(-sm.gbuf[(c + GR - 2) % GR][uc], G.z, z);
+            z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
+            z += sm.b1s[uc];
+            const float h = lc ? act_fwd_t<A1>(z) : 0.f;
+            // W2[o][uc] (pre-update: R6), kept for δ1 below
+            float wv[12];
+            {
+                const float4* wq = reinterpret_cast<const float4*>(&sm.w2s[uc][0]);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float4 f = wq[q];
+                    wv[4 * q] = f.x; wv[4 * q + 1] = f.y; wv[4 * q + 2] = f.z; wv[4 * q + 3] = f.w;
+                }
             }
-            const int o16 = lane & 15, hf = lane >> 4;
-            const bool valid = o16 < O;
-            float zsum = 0.f;
+            // ---- this warp's partial logits Σ_u W2[o][u] h_u: transpose-reduce over lanes ----
+            float pv0;
+            {
+                float pv[16];
 #pragma unroll
-            for (int i = 0; i < C * NWG / 2; ++i) zsum += gs.zbuf[pz][2 * i + hf][o16];
-            zsum += __shfl_xor_sync(0xffffffffu, zsum, 16);
-            const float b2o = sm.b2s[warp][o16];  // b2(t-1) (pad entries are 0)
-            const float z2 = zsum + b2o;           // z2 = W2 h + b2 (Eq.2)
-            const int label = sm.ylab[warp][(t + 63) & 63];         // y(t-1)
-            if constexpr (A2 == PNN_SOFTMAX) {
-                float m = valid ? z2 : -INFINITY;
+                for (int o = 0; o < 16; ++o) pv[o] = (o < O) ? wv[o < O ? o : 0] * h : 0.f;
+                const bool c4 = lane & 16, c3 = lane & 8, c2 = lane & 4, c1 = lane & 2;
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                const float e = valid ? __expf(z2 - m) : 0.f;
-                float sum = e;
+                for (int i = 0; i < 8; ++i)
+                    pv[i] = (c4 ? pv[i + 8] : pv[i]) + __shfl_xor_sync(0xffffffffu, c4 ? pv[i] : pv[i + 8], 16);
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                float inv;
-                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
-                dl = e * inv - ((o16 == label) ? 1.f : 0.f);
-            } else {
-                const float x2 = act_fwd_t<A2>(z2);
-                dl = (x2 - ((o16 == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
+                for (int i = 0; i < 4; ++i)
+                    pv[i] = (c3 ? pv[i + 4] : pv[i]) + __shfl_xor_sync(0xffffffffu, c3 ? pv[i] : pv[i + 4], 8);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    pv[i] = (c2 ? pv[i + 2] : pv[i]) + __shfl_xor_sync(0xffffffffu, c2 ? pv[i] : pv[i + 2], 4);
+                pv0 = (c1 ? pv[1] : pv[0]) + __shfl_xor_sync(0xffffffffu, c1 ? pv[0] : pv[1], 2);
+                pv0 += __shfl_xor_sync(0xffffffffu, pv0, 1);
             }
-            dl = valid ? dl : 0.f;
-            __syncwarp();                          // every lane has read b2s
-            if (lane < 16) sm.b2s[warp][lane] = fmaf(-lr, dl, b2o);   // b2(t)
-        }
-        // ---- δ1, g(t-1) of this lane's unit; W2(t), b1(t) ----
-        {
-            const float d0 = __shfl_sync(0xffffffffu, dl, tq);
-            const float d1 = __shfl_sync(0xffffffffu, dl, tq + 4);
-            const float d2 = __shfl_sync(0xffffffffu, dl, tq + 8);     // 0 for o = 10, 11
-            float s1 = fmaf(w2[2], d2, fmaf(w2[1], d1, w2[0] * d0));  // (W2ᵀδ2)_k, pre-update W2 (R6)
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-            const float gnew = tlive ? lr * (s1 * act_deriv_t<A1>(hprev)) : 0.f;   // g(t-1) = η δ1
-            w2[0] = fmaf(-(lr * d0), hprev, w2[0]);                     // W2(t)
-            w2[1] = fmaf(-(lr * d1), hprev, w2[1]);
-            w2[2] = fmaf(-(lr * d2), hprev, w2[2]);
-            b1 -= gnew;                            // b1(t)
-            gm2 = gm1;
-            gm1 = gnew;
-            if (tq == 0) gs.gw[(t + 1) & 1][wl][tr] = gnew;   // g(t-1), swept in U(t+1)
-        }
-        TR(4);
-        // ---- sample t: z1 = acc - g(t-2)G(t-2,t) - g(t-1)G(t-1,t) + b1(t); h; partial logits ----
-        if (t < T) {
-            const float2 G = *reinterpret_cast<const float2*>(xring + sx * DP + GOFF);
-            const float z1 = fmaf(-gm1, G.y, fmaf(-gm2, G.x, a)) + b1;
-            const float h = tlive ? act_fwd_t<A1>(z1) : 0.f;
-            hprev = h;
-            float pv[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                pv[i] = w2[i] * h;
-                pv[i] += __shfl_xor_sync(0xffffffffu, pv[i], 4);
-                pv[i] += __shfl_xor_sync(0xffffffffu, pv[i], 8);
-                pv[i] += __shfl_xor_sync(0xffffffffu, pv[i], 16);
-            }
-            const uint32_t zrow = (uint32_t)(crank * NWG + wl);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int o = lane + 4 * i;
-                const bool pub = lane < 4 && o < O;
-                if (pub) gs.zbuf[sz][zrow][o] = pv[i];
+            // lane l now holds output (l >> 1) = 8·c4 + 4·c3 + 2·c2 + c1
+            const int zs = c % ZS;
+            {
+                const int oi = lane >> 1;
+                const bool pub = (lane & 1) == 0 && oi < O;
+                if (pub) sm.zbuf[zs][zrow][oi] = pv0;
                 if constexpr (C > 1) {
 #pragma unroll
                     for (int p = 0; p < C - 1; ++p)
-                        st_async_f32_if(pub, rz[p] + sz * kZStride + o * 4, pv[i],
-                                        rz[p] + kZfullOff - zrow * 64u + sz * 8);
+                        st_async_f32_if(pub, rz[p] + zs * kZStride + oi * 4, pv0,
+                                        rz[p] + kZfullOff - (uint32_t)(zrow * 64) + zs * 8);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (C > 1) mbar_arrive_expect_tx(&sm.zfull[zs], (uint32_t)((C - 1) * O * 4));
+                    else mbar_arrive(&sm.zfull[zs]);
                 }
             }
-            // certify x(t+2) (and its Gram terms) for step t+2's F through zfull(t)
-            if (wl == 0 && t + 2 < T) {
-                const int s2 = (sx + 2 >= S) ? sx + 2 - S : sx + 2;
-                mbar_wait(&gs.xfull[s2], (sx + 2 >= S) ? (xpar ^ 1u) : xpar);
+            // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
+            //      which comes after their wait on gready(c) (first warp of the pair) ----
+            // every warp has passed U(c-1) (aready(c) above): the slot of x(c-1-L) is free for x(c+PF)
+            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
+            if (half == 0 && c + 2 + LAG < T) {
+                const int u = c + 2 + LAG;
+                mbar_wait(&sm.xfull[(cs + 2 + LAG) % S], (uint32_t)((u / S) & 1));
+            }
+            TR(4);
+            // ---- δ2(c) in every lane: z2 = Σ partials + b2(c) ----
+            mbar_wait(&sm.zfull[zs], (uint32_t)((c / ZS) & 1));
+            TR(5);
+            float dl[O];
+            {
+                float z2[12];
+                {
+                    const float4* bq = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const float4 f = bq[q];
+                        z2[4 * q] = f.x; z2[4 * q + 1] = f.y; z2[4 * q + 2] = f.z; z2[4 * q + 3] = f.w;
+                    }
+                }
+                float zp[12];
+#pragma unroll
+                for (int o = 0; o < 12; ++o) zp[o] = 0.f;
+#pragma unroll
+                for (int i = 0; i < 2 * C; ++i) {
+                    const float4* zq = reinterpret_cast<const float4*>(&sm.zbuf[zs][i][0]);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const float4 f = zq[q];
+                        zp[4 * q] += f.x; zp[4 * q + 1] += f.y; zp[4 * q + 2] += f.z; zp[4 * q + 3] += f.w;
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < 12; ++o) z2[o] += zp[o];                // z2 = W2 h + b2 (Eq.2)
+                if constexpr (A2 == PNN_SOFTMAX) {
+                    float m = z2[0];
+#pragma unroll
+                    for (int o = 1; o < O; ++o) m = fmaxf(m, z2[o]);
+                    float sum = 0.f;
+#pragma unroll
+                    for (int o = 0; o < O; ++o) { dl[o] = __expf(z2[o] - m); sum += dl[o]; }
+                    float inv;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
+                } else {
+#pragma unroll
+                    for (int o = 0; o < O; ++o) {
+                        const float x2 = act_fwd_t<A2>(z2[o]);
+                        dl[o] = (x2 - ((o == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
+                    }
+                }
+            }
+            // ---- δ1, g(c) of unit uc; W2(c+1), b1(c+1), b2(c+1) ----
+            {
+                float s1 = 0.f;                    // (W2ᵀδ2)_u with the pre-update W2 (R6)
+#pragma unroll
+                for (int o = 0; o < O; ++o) s1 = fmaf(wv[o], dl[o], s1);
+                const float gu = lc ? lr * (s1 * act_deriv_t<A1>(h)) : 0.f;   // g(c) = η δ1
+                sm.gbuf[c % GR][uc] = gu;
+                sm.b1s[uc] -= gu;
+#pragma unroll
+                for (int o = 0; o < O; ++o) wv[o] = fmaf(-(lr * dl[o]), h, wv[o]);
+                float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
+                wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+                wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
+                wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
+            }
+            if (half == 0 && lane == 0) {              // b2(c+1) into the other buffer: the pair's
+                const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);   // partner may
+                float4* bq = reinterpret_cast<float4*>(&sm.b2s[(c + 1) & 1][0]);        // still read b2(c)
+                const float4 b0 = bo[0], b1v = bo[1], b2v = bo[2];
+                bq[0] = make_float4(fmaf(-lr, dl[0], b0.x), fmaf(-lr, dl[1], b0.y), fmaf(-lr, dl[2], b0.z),
+                                    fmaf(-lr, dl[3], b0.w));
+                bq[1] = make_float4(fmaf(-lr, dl[4], b1v.x), fmaf(-lr, dl[5], b1v.y), fmaf(-lr, dl[6], b1v.z),
+                                    fmaf(-lr, dl[7], b1v.w));
+                bq[2] = make_float4(fmaf(-lr, dl[8], b2v.x), fmaf(-lr, dl[9], b2v.y), 0.f, 0.f);
             }
             __syncwarp();
-            if (lane == 0) {
-                if constexpr (C > 1) mbar_arrive_expect_tx(&gs.zfull[sz], (uint32_t)((C - 1) * O * 4));
-                else mbar_arrive(&gs.zfull[sz]);
-            }
+            if (lane == 0) mbar_arrive(&sm.gready[c % GR]);
+            TR(6);
         }
-        TR(5);
-        if (++sx == S) { sx = 0; xpar ^= 1u; }
-        pz = sz;
-        ppar = zpar;
-        if (++sz == ZS) { sz = 0; zpar ^= 1u; }
+        if (++sx == S) sx = 0;
     }
 #undef TR
 
     // ---- write back ----
-    if (active) {
-        float* W1o = opaque(W1);
+    float* W1o = opaque(W1);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            if (kr0 + r < Uown) {
-                float* dst = W1o + (long long)(k0 + kr0 + r) * D;
+    for (int r = 0; r < R; ++r) {
+        if (kr0 + r < Uown) {
+            float* dst = W1o + (long long)(k0 + kr0 + r) * D;
 #pragma unroll
-                for (int m = 0; m < NP; ++m) *reinterpret_cast<uint64_t*>(dst + pcol(lane, m)) = w[r][m];
-            }
+            for (int m = 0; m < NP; ++m) *reinterpret_cast<uint64_t*>(dst + pcol(lane, m)) = w[r][m];
         }
-        if (tlive) {
-            const float4 w4 = *reinterpret_cast<const float4*>(wxp);
-            float* dst = W1o + (long long)ku * D + XC + 4 * tq;
-            if (nx > 0) dst[0] = w4.x;
-            if (nx > 1) dst[1] = w4.y;
-            if (nx > 2) dst[2] = w4.z;
-            if (nx > 3) dst[3] = w4.w;
-            float* W2o = opaque(W2);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int o = tq + 4 * i;
-                if (o < O) W2o[(long long)o * H + ku] = w2[i];
-            }
-            if (tq == 0) opaque(b1g)[ku] = b1;
-        }
-        if (crank == 0 && wl == 0 && lane < O) opaque(b2g)[lane] = sm.b2s[warp][lane];
     }
-    __syncthreads();
+    if (xlive) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wxp);
+        float* dst = W1o + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
+        if (nx > 0) dst[0] = w4.x;
+        if (nx > 1) dst[1] = w4.y;
+        if (nx > 2) dst[2] = w4.z;
+        if (nx > 3) dst[3] = w4.w;
+    }
+    __syncthreads();                               // the last chain's W2 / b1 / b2 are in shared memory
+    float* W2o = opaque(W2);
+    for (int i = threadIdx.x; i < Uown * O; i += blockDim.x) {
+        const int u = i / O, o = i % O;
+        W2o[(long long)o * H + k0 + u] = sm.w2s[u][o];
+    }
+    for (int i = threadIdx.x; i < Uown; i += blockDim.x) opaque(b1g)[k0 + i] = sm.b1s[i];
+    if (crank == 0 && threadIdx.x < O) opaque(b2g)[threadIdx.x] = sm.b2s[T & 1][threadIdx.x];
     if constexpr (C > 1) cluster_sync_all();       // no CTA leaves while a peer may still st.async into it
 }
 
-template <int C, int NG, int A1, int A2, bool TRACE>
+template <int C, int A1, int A2, bool TRACE>
 cudaError_t launch_one(const ResidentPlan& p, const NetDesc& d, float* children, const float* x,
-                       const int32_t* labels, float4* gram, long long n_local, int K_local, int s_first,
-                       int s_count, float lr, cudaStream_t st) {
-    auto kern = sgd_resident_kernel<C, NG, A1, A2, TRACE>;
+                       const float4* rec, long long n_local, int K_local, int s_first, int s_count,
+                       float lr, cudaStream_t st) {
+    auto kern = sgd_resident_kernel<C, A1, A2, TRACE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    const int clusters = (s_count + NG - 1) / NG;
-    cfg.gridDim = dim3((unsigned)(clusters * C));
+    cfg.gridDim = dim3((unsigned)(s_count * C));
     cfg.blockDim = dim3((unsigned)p.threads);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
@@ -522,20 +550,19 @@ cudaError_t launch_one(const ResidentPlan& p, const NetDesc& d, float* children,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, d, children, x, labels, (const float4*)gram, n_local, K_local,
-                              s_first, s_count, lr, g_trace);
+    return cudaLaunchKernelEx(&cfg, kern, d, children, x, rec, n_local, K_local, s_first, lr, g_trace);
 }
 
-template <int C, int NG>
-cudaError_t launch_cg(const ResidentPlan& p, const NetDesc& d, float* children, const float* x,
-                      const int32_t* labels, float4* gram, long long n_local, int K_local, int s_first,
-                      int s_count, float lr, cudaStream_t st) {
+template <int C>
+cudaError_t launch_c(const ResidentPlan& p, const NetDesc& d, float* children, const float* x,
+                     const float4* rec, long long n_local, int K_local, int s_first, int s_count,
+                     float lr, cudaStream_t st) {
 #define PNN_ACTS(A1_, A2_)                                                                        \
     if (d.act[0] == A1_ && d.act[1] == A2_)                                                     \
-        return g_trace ? launch_one<C, NG, A1_, A2_, true>(p, d, children, x, labels, gram, n_local, K_local, \
-                                                           s_first, s_count, lr, st)              \
-                       : launch_one<C, NG, A1_, A2_, false>(p, d, children, x, labels, gram, n_local, K_local, \
-                                                            s_first, s_count, lr, st);
+        return g_trace ? launch_one<C, A1_, A2_, true>(p, d, children, x, rec, n_local, K_local, s_first, \
+                                                       s_count, lr, st)                           \
+                       : launch_one<C, A1_, A2_, false>(p, d, children, x, rec, n_local, K_local, s_first, \
+                                                        s_count, lr, st);
     PNN_ACTS(PNN_RELU, PNN_SOFTMAX)
     PNN_ACTS(PNN_TANH, PNN_SOFTMAX)
     PNN_ACTS(PNN_SIGMOID, PNN_SOFTMAX)
@@ -567,42 +594,29 @@ ResidentPlan plan_resident(const NetDesc& d, int batch) {
                        (a1 == PNN_SIGMOID && a2 == PNN_SOFTMAX) || (a1 == PNN_SIGMOID && a2 == PNN_SIGMOID) ||
                        (a1 == PNN_TANH && a2 == PNN_TANH) || (a1 == PNN_RELU && a2 == PNN_SIGMOID);
     if (!built) return no("activation pair not instantiated in the resident kernel");
-    // groups per CTA: PNN_RESIDENT_GROUPS=2 puts two CNs on every SM (cluster twice as wide)
-    const char* env = getenv("PNN_RESIDENT_GROUPS");
-    int ng = (env && atoi(env) == 2) ? 2 : 1;
     int c = 1;
-    while (c <= CMAX && (H + c - 1) / c > R * (NWMAX / ng)) c *= 2;
-    if (c > CMAX && ng == 2) {                     // too wide for two groups: one group per CTA
-        ng = 1;
-        c = 1;
-        while (c <= CMAX && (H + c - 1) / c > R * NWMAX) c *= 2;
-    }
+    while (c <= CMAX && (H + c - 1) / c > UMAX) c *= 2;
     if (c > CMAX) return no("hidden layer wider than 256");
-    const int U = (H + c - 1) / c;
     p.cluster = c;
-    p.groups = ng;
-    (void)U;
-    p.threads = NWMAX * 32;                        // NWMAX/ng warps per group; rows >= U are idle
-    p.smem = kSmemHead + sizeof(float) * (size_t)ng * (S + 1) * DP;
-    p.variant = 7;
+    p.groups = 1;
+    p.threads = NW * 32;                           // 8 warps; rows >= U are idle
+    p.smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
+    p.variant = 8;
     p.ok = true;
     return p;
 }
 
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
-                                const float* x, const int32_t* labels, float4* gram, long long n_local,
+                                const float* x, const int32_t* labels, float4* rec, long long n_local,
                                 int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
     if (s_count <= 0) return cudaSuccess;
-    gram_kernel<<<592, 256, 0, st>>>(x, d.n[0], n_local, K_local, s_first, s_count, gram);
+    gram_kernel<<<592, 256, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    switch (p.cluster * 10 + p.groups) {
-    case 11: return launch_cg<1, 1>(p, d, children, x, labels, gram, n_local, K_local, s_first, s_count, lr, st);
-    case 21: return launch_cg<2, 1>(p, d, children, x, labels, gram, n_local, K_local, s_first, s_count, lr, st);
-    case 41: return launch_cg<4, 1>(p, d, children, x, labels, gram, n_local, K_local, s_first, s_count, lr, st);
-    case 12: return launch_cg<1, 2>(p, d, children, x, labels, gram, n_local, K_local, s_first, s_count, lr, st);
-    case 22: return launch_cg<2, 2>(p, d, children, x, labels, gram, n_local, K_local, s_first, s_count, lr, st);
-    case 42: return launch_cg<4, 2>(p, d, children, x, labels, gram, n_local, K_local, s_first, s_count, lr, st);
+    switch (p.cluster) {
+    case 1: return launch_c<1>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+    case 2: return launch_c<2>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+    case 4: return launch_c<4>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -170,7 +170,7 @@ pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long
             cudaFree(net->d_gram);
             net->d_gram = nullptr;
             net->gram_rows = 0;
-            CUDA_TRY(net, cudaMalloc(&net->d_gram, sizeof(float4) * (size_t)n));
+            CUDA_TRY(net, cudaMalloc(&net->d_gram, 2 * sizeof(float4) * (size_t)n));   // 32-B records
             net->gram_rows = n;
         }
         e = launch_sgd_resident(plan, net->d, net->d_children, x, y, net->d_gram, n, net->K_local,

@@ -51,7 +51,8 @@ struct ResidentPlan {
     char why[160];      // reason when !ok
 };
 ResidentPlan plan_resident(const NetDesc& d, int batch);
-// gram: scratch of n_local float4 (the lookahead's Gram terms, recomputed per call).
+// gram: scratch of 2·n_local float4 (32-B records: the lookahead's Gram terms and the
+// label of every row, recomputed per call).
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
                                 const float* x, const int32_t* labels, float4* gram, long long n_local,
                                 int K_local, int s_first, int s_count, float lr,

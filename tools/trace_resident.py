@@ -1,9 +1,9 @@
-"""clock64 timeline of the resident kernel (v7), first two CTAs: per warp and
-step t, points 0 loop top, 1 after F(t), 2 after U(t), 3 after the zfull
-wait, 4 after finishing sample t-1, 5 after publishing sample t.
+"""clock64 timeline of the resident kernel (v8), first two CTAs: per warp and
+step s, points 0 loop top, 1 after F(s), 2 after U(s); for the warp that runs
+the chain of sample s-1: 3 after its waits (row sums, previous chain), 4 after
+publishing its partial logits, 5 after the exchange wait, 6 chain done.
 
-    python tools/trace_resident.py --config C4 --K 2 --rows 256
-(PNN_RESIDENT_GROUPS=2 selects two CNs per CTA.)
+    python tools/trace_resident.py --config C4 --K 1 --rows 256
 """
 import argparse
 import ctypes
@@ -20,7 +20,7 @@ from workloads import CONFIGS  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
-ap.add_argument("--K", type=int, default=2)
+ap.add_argument("--K", type=int, default=1)
 ap.add_argument("--rows", type=int, default=256)
 a = ap.parse_args()
 c = CONFIGS[a.config]
@@ -37,19 +37,33 @@ net.train_epoch(xd, yd)
 torch.cuda.synchronize()
 L.pnn_debug_set_trace(None)
 tr = buf.cpu().numpy().reshape(2, NW, TT, PP).astype(np.float64)
-names = ["top", "F", "U", "zwait", "finish(t-1)", "publish(t)"]
 for cta in range(2):
     for w in range(NW):
         T = tr[cta, w, 16:48]
         if not T[:, 0].any():
             continue
         per = np.diff(T[:, 0]).mean()
-        seg = [(T[:, i + 1] - T[:, i]).mean() for i in range(5)]
-        print(f"cta {cta} warp {w}: period {per:.0f} | " +
-              " ".join(f"{names[i]}->{names[i+1]} {seg[i]:.0f}" for i in range(5)) +
-              f" | publish->next top {np.mean(T[1:, 0] - T[:-1, 5]):.0f}")
-base = tr[0, 0, 20, 0]
-print("step 20 timeline (cycles from cta0 warp0's step-20 top):")
-for cta in range(2):
-    for w in range(NW):
-        print(f"  cta {cta} w{w}: " + " ".join(f"{tr[cta, w, 20, i] - base:6.0f}" for i in range(6)))
+        f, u = (T[:, 1] - T[:, 0]).mean(), (T[:, 2] - T[:, 1]).mean()
+        ch = T[T[:, 3] > 0]
+        cs = ""
+        if len(ch):
+            cs = (f" | chain: wait {np.mean(ch[:, 3] - ch[:, 2]):.0f} publish {np.mean(ch[:, 4] - ch[:, 3]):.0f}"
+                  f" xwait {0:.0f} exch {np.mean(ch[:, 5] - ch[:, 4]):.0f} finish {np.mean(ch[:, 6] - ch[:, 5]):.0f}")
+        print(f"cta {cta} warp {w}: period {per:.0f} | F {f:.0f} U {u:.0f}{cs}")
+# chain period: time between consecutive chain completions (point 6 of the owning warp)
+done = []
+for s in range(17, 48):
+    w = (s - 1) % NW
+    if tr[0, w, s, 6] > 0:
+        done.append(tr[0, w, s, 6])
+if len(done) > 2:
+    print(f"chain period (cta 0): {np.diff(done).mean():.0f} cycles/sample")
+print("per-sample chain timeline, cta 0 (cycles rel. to first): c, pair warps: [TR2 (ready to start), TR3 (waits done), TR4, TR5, TR6] for warp A | B")
+rows = []
+for cc in range(20, 30):
+    s = cc + 1
+    wa = 2 * (cc & 3)
+    rows.append((cc, [tr[0, wa, s, i] for i in (2, 3, 4, 5, 6)], [tr[0, wa + 1, s, i] for i in (2, 3, 4, 5, 6)]))
+t0 = rows[0][1][1]
+for cc, A, B in rows:
+    print(f"  c={cc}: A " + " ".join(f"{v - t0:7.0f}" for v in A) + " | B " + " ".join(f"{v - t0:7.0f}" for v in B))
