@@ -265,6 +265,10 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     int sx = 0;                                    // ring slot of x(s) = s % S
     for (int s = 0; s <= T + LAG; ++s) {
         TR(0);
+        // warps 4..7 (the sub-partition partners of warps 0..3) run U before F: the two sweeps
+        // of a sub-partition are then out of phase, and those rows' F(s) sees g(s-L) already
+        // applied (one correction term fewer in the chain)
+        if (warp < 4) {
         if (s < T) {
             // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
             if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
@@ -315,11 +319,13 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
         }
-        TR(1);
+            TR(1);
         if (s >= LAG && s - LAG < T) {
             // ---------------- U(s): W¹ -= g(s-L)·x(s-L)ᵀ ----------------
             const int u = s - LAG;
+#ifndef PNN_EXP_NO_GWAIT
             mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+#endif
             const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
             const float* xo = xring + su * DP + 4 * lane;
             const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
@@ -346,11 +352,100 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
             *reinterpret_cast<float4*>(wxp) = w4;
         }
+        } else {
+        if (s >= LAG && s - LAG < T) {
+            // ---------------- U(s): W¹ -= g(s-L)·x(s-L)ᵀ ----------------
+            const int u = s - LAG;
+#ifndef PNN_EXP_NO_GWAIT
+            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+#endif
+            const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
+            const float* xo = xring + su * DP + 4 * lane;
+            const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
+            const float4 g0 = gv[0], g1 = gv[1];
+            const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
+            uint64_t xa, xb;
+            lds4(xo, xa, xb);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t na = 0ull, nb = 0ull;
+                if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
+                    w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
+                }
+                xa = na;
+                xb = nb;
+            }
+            float4 w4 = *reinterpret_cast<const float4*>(wxp);
+            const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
+            const float gq = -sm.gbuf[u % GR][kr0 + tr];
+            w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
+            w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
+            *reinterpret_cast<float4*>(wxp) = w4;
+        }
+        if (s < T) {
+            // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
+            if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
+            // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
+            const float* xn = xring + sx * DP + 4 * lane;
+            uint64_t acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = 0ull;
+            uint64_t xa, xb;
+            lds4(xn, xa, xb);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t na = 0ull, nb = 0ull;
+                if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);   // one quad ahead
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
+                    acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
+                }
+                xa = na;
+                xb = nb;
+            }
+            float px;                              // columns 768..783 of row tr
+            {
+                const float4 w4 = *reinterpret_cast<const float4*>(wxp);
+                const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
+                px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
+            }
+            float v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float lo, hi;
+                upk(acc[r], lo, hi);
+                v[r] = lo + hi;
+            }
+            // transpose-reduce 8 row sums over lanes 16/8/4: row (lane >> 2), part (lane & 3)
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+            float u4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+            float u2[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
+            const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
+            sm.asum[s % AR][kr0 + tr][tq] = part;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
+        }
+            TR(1);
+        }
         TR(2);
 
         // ================= the chain of sample c = s - 1 (a pair of warps per sample) =================
         const int c = s - 1;
+#ifdef PNN_EXP_NO_CHAIN
+        if (false) {
+#else
         if (c >= 0 && c < T && (c & 3) == (warp >> 1)) {
+#endif
             const int cs = (sx >= 1) ? sx - 1 : S - 1;          // ring slot of x(c)
             mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));   // every warp's row sums of c
             if (c >= 1) mbar_wait(&sm.gready[(c - 1) % GR], (uint32_t)(((c - 1) / GR) & 1));   // chain c-1
@@ -360,7 +455,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             const int label = __float_as_int(xring[cs * DP + GOFF + 4]);
             const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][uc][0]);
             float z = (pa.x + pa.y) + (pa.z + pa.w);
-            z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);
+            if (half == 0) z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);   // rows of warps 0..3
             z = fmaf(-sm.gbuf[(c + GR - 3) % GR][uc], G.y, z);
             z = fmaf(-sm.gbuf[(c + GR - 2) % GR][uc], G.z, z);
             z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
