@@ -113,9 +113,11 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
 
 // Gram record of every row of CNs [s_first, s_first + s_count) (shard-local index u):
 // rec[2·row] = {x(u-4)·x(u), x(u-3)·x(u), x(u-2)·x(u), x(u-1)·x(u)} (0 before the slice
-// start), rec[2·row + 1] = {label bits, 0, 0, 0}.  One warp per row; X is read once from
-// HBM (the four previous rows hit in cache).
-__global__ void __launch_bounds__(256)
+// start), rec[2·row + 1] = {label bits, 0, 0, 0}.  A warp walks a chunk of GCH consecutive
+// rows keeping the last four rows in registers (lane l: columns 4l + 128q, q < 6, and
+// 768 + 4l for l < 4), so X is read from HBM about once.
+constexpr int GCH = 32;
+__global__ void __launch_bounds__(128)
 gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, long long n_local,
             int K_local, int s_first, int s_count, float4* __restrict__ rec) {
     long long r0, c0, r1, c1;
@@ -125,31 +127,67 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
     const int lane = threadIdx.x & 31;
     const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
     const long long base = n_local / K_local, rem = n_local % K_local;
-    for (long long i = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < rows; i += nwarps) {
-        const long long row = r0 + i;
-        // the CN owning this row (R17: the first rem slices are one row longer)
+    auto shard_start = [&](long long row) {       // first row of the CN owning `row` (R17)
         const long long s = (row < rem * (base + 1)) ? row / (base + 1)
                                                      : rem + (row - rem * (base + 1)) / base;
         long long st, cnt;
         shard_of(n_local, K_local, (int)s, &st, &cnt);
-        const long long u = row - st;
-        const float* xc = X + row * (long long)D;
-        float gk[4] = {0.f, 0.f, 0.f, 0.f};        // gk[4-k] = x(u-k)·x(u)
-        for (int j = lane * 4; j < D; j += 128) {
-            const float4 c = *reinterpret_cast<const float4*>(xc + j);
+        return st;
+    };
+    auto load = [&](long long row, float4 (&v)[7]) {
+        const float* xr = X + row * (long long)D;
 #pragma unroll
-            for (int k = 1; k <= 4; ++k) {
-                if (u >= k) {
-                    const float4 b = *reinterpret_cast<const float4*>(xc - k * D + j);
-                    gk[4 - k] = fmaf(b.w, c.w, fmaf(b.z, c.z, fmaf(b.y, c.y, fmaf(b.x, c.x, gk[4 - k]))));
-                }
-            }
+        for (int q = 0; q < 6; ++q) v[q] = *reinterpret_cast<const float4*>(xr + 4 * lane + 128 * q);
+        v[6] = (4 * lane + 768 < D) ? *reinterpret_cast<const float4*>(xr + 768 + 4 * lane)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto dot = [](const float4 (&a)[7], const float4 (&b)[7]) {
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+            s = fmaf(a[q].w, b[q].w, fmaf(a[q].z, b[q].z, fmaf(a[q].y, b[q].y, fmaf(a[q].x, b[q].x, s))));
+        return s;
+    };
+    const long long nchunks = (rows + GCH - 1) / GCH;
+    for (long long ch = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
+        const long long a0 = r0 + ch * GCH, a1 = min(a0 + GCH, r0 + rows);
+        float4 win[4][7];                          // win[k] = x(row - 4 + k), k = 0..3
+        const long long st = shard_start(a0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const long long pr = a0 - 4 + k;
+            if (pr >= st) load(pr, win[k]);
+            else
+#pragma unroll
+                for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        float4 nxt[7];
+        load(a0, nxt);
+        for (long long row = a0; row < a1; ++row) {
+            const long long s0 = shard_start(row);
+            if (s0 == row && row != a0) {          // a new slice begins: no terms before it
 #pragma unroll
-        for (int k = 0; k < 4; ++k) gk[k] = warp_sum(gk[k]);
-        if (lane == 0) {
-            rec[2 * row] = make_float4(gk[0], gk[1], gk[2], gk[3]);
-            rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), 0.f, 0.f, 0.f);
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float4 cur[7];
+#pragma unroll
+            for (int q = 0; q < 7; ++q) cur[q] = nxt[q];
+            if (row + 1 < a1) load(row + 1, nxt);  // one row ahead
+            float gk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gk[k] = warp_sum(dot(win[k], cur));
+            if (lane == 0) {
+                rec[2 * row] = make_float4(gk[0], gk[1], gk[2], gk[3]);
+                rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int q = 0; q < 7; ++q) win[k][q] = win[k + 1][q];
+#pragma unroll
+            for (int q = 0; q < 7; ++q) win[3][q] = cur[q];
         }
     }
 }
@@ -705,7 +743,7 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 const float* x, const int32_t* labels, float4* rec, long long n_local,
                                 int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
     if (s_count <= 0) return cudaSuccess;
-    gram_kernel<<<592, 256, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
+    gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     switch (p.cluster) {
