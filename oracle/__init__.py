@@ -74,6 +74,10 @@ def lib():
         L.orc_init.argtypes = [P, I, I, ctypes.c_uint64, P]
         L.orc_init.restype = I
         L.orc_param_count.argtypes = [P, I]
+        L.orc_bf16_round.argtypes = [ctypes.c_float]
+        L.orc_bf16_round.restype = ctypes.c_float
+        L.orc_train_bf16.argtypes = [P, I, P, P, P, P, ctypes.c_long, ctypes.c_float, I, I]
+        L.orc_train_bf16.restype = I
         L.orc_param_count.restype = ctypes.c_long
         L.orc_shard_bounds.argtypes = [ctypes.c_long, I, P, P]
         L.orc_shard_bounds.restype = None
@@ -165,9 +169,27 @@ def cost(layers, act, params, x0, label, dtype=np.float64) -> float:
                                            int(label), _p(scratch))
 
 
-def train(layers, act, params, X, y, lr, epochs=1, batch=1, dtype=np.float32) -> np.ndarray:
-    """Train ONE network over rows X in order; returns the new parameters."""
+def bf16_round(v: float) -> float:
+    """bfloat16 round-to-nearest-even of one fp32 value (reading R25)."""
+    return float(lib().orc_bf16_round(float(v)))
+
+
+def train(layers, act, params, X, y, lr, epochs=1, batch=1, dtype=np.float32,
+          precision="fp32") -> np.ndarray:
+    """Train ONE network over rows X in order; returns the new parameters.
+    precision="bf16": the mini-batch variant with R25's bf16 rounding points
+    (fp32 master weights, fp32 accumulation); always fp32 arithmetic."""
     layers, act, L = _net(layers, act)
+    if precision == "bf16":
+        out = np.array(params, dtype=np.float32, copy=True)
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        y = np.ascontiguousarray(y, dtype=np.int32)
+        assert X.shape == (len(y), layers[0])
+        rc = lib().orc_train_bf16(_p(layers), L, _p(act), _p(out), _p(X), _p(y), len(y), float(lr),
+                                  int(epochs), int(batch))
+        if rc != 0:
+            raise MemoryError("oracle allocation failed")
+        return out
     dtype, suf = _dt(dtype)
     out = np.array(params, dtype=dtype, copy=True)
     X = np.ascontiguousarray(X, dtype=dtype)
@@ -210,7 +232,7 @@ def merge(children: np.ndarray) -> np.ndarray:
 
 
 def train_pnn(layers, act, init, K, lr, seed, X, y, epochs=1, batch=1, dtype=np.float32,
-              threads=1, subnets=None, init_params_=None):
+              threads=1, subnets=None, init_params_=None, precision="fp32"):
     """The paper's PNN procedure.  Returns (children [K or len(subnets), P], merged or None).
 
     ``subnets`` restricts training to those child indices (full-size sampled
@@ -223,7 +245,7 @@ def train_pnn(layers, act, init, K, lr, seed, X, y, epochs=1, batch=1, dtype=np.
     if N is None:
         raise ValueError("pass N via X arrays, or use train_pnn_rows")
     return _train_children(layers, act, p0, K, lr, N, lambda s, c: (X[s:s + c], y[s:s + c]),
-                           epochs, batch, dtype, threads, subnets)
+                           epochs, batch, dtype, threads, subnets, precision)
 
 
 def train_pnn_rows(layers, act, init, K, lr, seed, N, rows, epochs=1, batch=1,
@@ -232,13 +254,14 @@ def train_pnn_rows(layers, act, init, K, lr, seed, N, rows, epochs=1, batch=1,
     return _train_children(layers, act, p0, K, lr, N, rows, epochs, batch, dtype, threads, subnets)
 
 
-def _train_children(layers, act, p0, K, lr, N, rows, epochs, batch, dtype, threads, subnets):
+def _train_children(layers, act, p0, K, lr, N, rows, epochs, batch, dtype, threads, subnets,
+                    precision="fp32"):
     start, count = shard_bounds(N, K)
     idx = list(range(K)) if subnets is None else list(subnets)
 
     def one(i):
         Xi, yi = rows(int(start[i]), int(count[i]))
-        return train(layers, act, p0, Xi, yi, lr, epochs, batch, dtype).astype(np.float32)
+        return train(layers, act, p0, Xi, yi, lr, epochs, batch, dtype, precision).astype(np.float32)
 
     if threads > 1:
         with ThreadPoolExecutor(max_workers=threads) as ex:

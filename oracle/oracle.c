@@ -51,6 +51,132 @@ enum { ORC_INIT_NORMAL = 0, ORC_INIT_UNIFORM = 1, ORC_INIT_XAVIER = 2, ORC_INIT_
 #undef EXP
 #undef TANH
 
+/* ---- bf16 mini-batch variant (a10; north_star "bf16 weights and activations
+ * with fp32 accumulate and fp32 master weights"; reading R25) ---------------
+ * bf16(v): round-to-nearest-even to the 8-bit-mantissa bfloat16, returned as a
+ * float.  NaN is kept quiet.                                                 */
+float orc_bf16_round(float v) {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) {
+        u |= 0x00400000u;                       /* quiet NaN */
+    } else {
+        u += 0x7fffu + ((u >> 16) & 1u);        /* RNE on the low 16 bits */
+    }
+    u &= 0xffff0000u;
+    float r;
+    memcpy(&r, &u, 4);
+    return r;
+}
+
+/* Mini-batch GD (the gradients of the batch are averaged before
+ * one update; short last batch averaged over its size, R14) with the rounding
+ * points of reading R25, for one network over rows X[0..n):
+ *   per step:  Wb^l = bf16(W^l) (fp32 master W), weights fixed over the batch;
+ *   forward:   xb^0 = bf16(x); z^l_k = Σ_j Wb^l_kj xb^{l-1}_j (fp32, ascending j) + b^l_k;
+ *              x^l = φ(z^l) in fp32 (softmax max-subtracted, R4); hidden layers
+ *              pass xb^l = bf16(x^l) on;
+ *   deltas:    δ^L = x^L - e (softmax+CE) or (x^L - e)⊙φ'(x^L); δb = bf16(δ);
+ *              δ^l_j = (Σ_k Wb^{l+1}_kj δb^{l+1}_k) ⊙ φ'(x^l_j) (pre-update weights, R6);
+ *   gradient:  G^l_kj += δb^l_k xb^{l-1}_j (fp32), gb^l_k += δ^l_k (fp32);
+ *   update:    W ← W - η·(G / B_actual), b ← b - η·(gb / B_actual)  (fp32).      */
+int orc_train_bf16(const int* layers, int L, const int* act, float* params, const float* X,
+                   const int* y, long n, float lr, int epochs, int batch) {
+    long woff[ORC_MAX_LAYERS + 1], noff[ORC_MAX_LAYERS + 1];
+    long w = 0, nn = 0;
+    for (int l = 1; l <= L; ++l) {
+        woff[l] = w;
+        noff[l] = nn;
+        w += (long)layers[l] * layers[l - 1] + layers[l];
+        nn += layers[l];
+    }
+    const long P = w, tot = nn;
+    const int d0 = layers[0];
+    float* Wb = (float*)malloc(sizeof(float) * P);
+    float* G = (float*)malloc(sizeof(float) * P);
+    float* xs = (float*)malloc(sizeof(float) * tot);   /* x^l (fp32)           */
+    float* xb = (float*)malloc(sizeof(float) * tot);   /* bf16(x^l)            */
+    float* ds = (float*)malloc(sizeof(float) * tot);   /* δ^l (fp32)           */
+    float* db = (float*)malloc(sizeof(float) * tot);   /* bf16(δ^l)            */
+    float* x0b = (float*)malloc(sizeof(float) * d0);
+    if (!Wb || !G || !xs || !xb || !ds || !db || !x0b) {
+        free(Wb); free(G); free(xs); free(xb); free(ds); free(db); free(x0b);
+        return -1;
+    }
+    if (batch < 1) batch = 1;
+    for (int e = 0; e < epochs; ++e) {
+        for (long t0 = 0; t0 < n; t0 += batch) {
+            const long bsz = (n - t0 < batch) ? (n - t0) : batch;
+            for (long i = 0; i < P; ++i) { Wb[i] = orc_bf16_round(params[i]); G[i] = 0.f; }
+            for (long t = t0; t < t0 + bsz; ++t) {
+                for (int j = 0; j < d0; ++j) x0b[j] = orc_bf16_round(X[t * d0 + j]);
+                /* forward */
+                for (int l = 1; l <= L; ++l) {
+                    const int nin = layers[l - 1], nout = layers[l];
+                    const float* W = Wb + woff[l];
+                    const float* b = params + woff[l] + (long)nout * nin;   /* fp32 bias */
+                    const float* xin = (l == 1) ? x0b : xb + noff[l - 1];
+                    float* x = xs + noff[l];
+                    for (int k = 0; k < nout; ++k) {
+                        float acc = 0.f;
+                        for (int j = 0; j < nin; ++j) acc += W[(long)k * nin + j] * xin[j];
+                        x[k] = acc + b[k];                                  /* z, then φ */
+                    }
+                    if (act[l - 1] == ORC_SOFTMAX) {
+                        float m = x[0];
+                        for (int k = 1; k < nout; ++k) if (x[k] > m) m = x[k];
+                        float s = 0.f;
+                        for (int k = 0; k < nout; ++k) { x[k] = expf(x[k] - m); s += x[k]; }
+                        for (int k = 0; k < nout; ++k) x[k] = x[k] / s;
+                    } else {
+                        for (int k = 0; k < nout; ++k) x[k] = act_scalar_f32(act[l - 1], x[k]);
+                    }
+                    for (int k = 0; k < nout; ++k) xb[noff[l] + k] = orc_bf16_round(x[k]);
+                }
+                /* deltas */
+                {
+                    const int nL = layers[L];
+                    const float* xo = xs + noff[L];
+                    for (int i = 0; i < nL; ++i) {
+                        const float ev = (i == y[t]) ? 1.f : 0.f;
+                        float d = (act[L - 1] == ORC_SOFTMAX)
+                                      ? xo[i] - ev
+                                      : (xo[i] - ev) * act_deriv_from_x_f32(act[L - 1], xo[i]);
+                        ds[noff[L] + i] = d;
+                        db[noff[L] + i] = orc_bf16_round(d);
+                    }
+                    for (int l = L - 1; l >= 1; --l) {
+                        const int nh = layers[l], nn2 = layers[l + 1];
+                        const float* Wn = Wb + woff[l + 1];
+                        for (int j = 0; j < nh; ++j) {
+                            float acc = 0.f;
+                            for (int k = 0; k < nn2; ++k) acc += Wn[(long)k * nh + j] * db[noff[l + 1] + k];
+                            const float d = acc * act_deriv_from_x_f32(act[l - 1], xs[noff[l] + j]);
+                            ds[noff[l] + j] = d;
+                            db[noff[l] + j] = orc_bf16_round(d);
+                        }
+                    }
+                }
+                /* gradient sums */
+                for (int l = 1; l <= L; ++l) {
+                    const int nin = layers[l - 1], nout = layers[l];
+                    float* Gl = G + woff[l];
+                    float* gb = Gl + (long)nout * nin;
+                    const float* xin = (l == 1) ? x0b : xb + noff[l - 1];
+                    for (int k = 0; k < nout; ++k) {
+                        const float dk = db[noff[l] + k];
+                        for (int j = 0; j < nin; ++j) Gl[(long)k * nin + j] += dk * xin[j];
+                        gb[k] += ds[noff[l] + k];
+                    }
+                }
+            }
+            for (long i = 0; i < P; ++i) params[i] -= lr * (G[i] / (float)bsz);
+        }
+    }
+    free(Wb); free(G); free(xs); free(xb); free(ds); free(db); free(x0b);
+    return 0;
+}
+
 /* ---- init (reading R15) ------------------------------
  * Counter-based: uniform u(seed, layer, kind, index, s) with
  *   ctr = (layer << 48) ^ (kind << 47) ^ (2*index + s)
