@@ -79,7 +79,10 @@ enum { PNN_FP32 = 0, PNN_BF16 = 1 };
 /* Training kernel selection (pnn_set_kernel). */
 enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          */
        PNN_KERNEL_REFERENCE = 1, /* one CTA per CN, weights in global memory    */
-       PNN_KERNEL_RESIDENT = 2   /* persistent cluster kernel, on-chip weights  */ };
+       PNN_KERNEL_RESIDENT = 2,  /* persistent cluster kernel, on-chip weights  */
+       PNN_KERNEL_TC_BF16 = 3    /* bf16 mini-batch on tcgen05 GEMMs; chosen by
+                                    pnn_set_minibatch(.., PNN_BF16), reported
+                                    by pnn_kernel_info, not settable         */ };
 
 /* Build a PNN of n_subnets CNs with layer sizes layers[0..n_layers-1]
  * (layers[0] = inputs, e.g. {784,128,10}; n_layers >= 2, each size >= 1,
@@ -111,8 +114,12 @@ pnn_status pnn_set_comm(pnn_net net, const void* nccl_unique_id, int32_t nranks,
  * update after every instance); batch > 1 is mini-batch GD (gradients of the
  * batch averaged before one update; the short last batch of a slice is
  * averaged over its actual size, R14).  precision PNN_FP32 or PNN_BF16 (bf16
- * operands, fp32 accumulate + master weights; requires batch > 1).
- * Errors: PNN_ERR_INVALID (batch < 1, unknown / unsupported precision).     */
+ * operands, fp32 accumulate + master weights, rounding points of DESIGN.md
+ * §3 R25; built for D-H1-H2-O nets with ReLU, ReLU, softmax, batch 64,
+ * D % 8 == 0, H1 % 128 == 0, H2 % 256 == 0, O <= 16 — the C5 shape
+ * 784-1024-1024-10; it then overrides pnn_set_kernel).
+ * Errors: PNN_ERR_INVALID (batch < 1, unknown precision, PNN_BF16 on a shape
+ * outside the list above — the message names the violated condition).     */
 pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision);
 
 /* Force a training kernel (PNN_KERNEL_*).  PNN_KERNEL_RESIDENT returns
@@ -178,7 +185,9 @@ int64_t pnn_param_count(pnn_net net);
 pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count);
 
 /* Which training kernel the next pnn_train_epoch launches (PNN_KERNEL_*),
- * and how many kernel launches it makes.  Errors: PNN_ERR_INVALID.          */
+ * and how many kernel launches it makes (PNN_KERNEL_TC_BF16: launches per
+ * mini-batch step; an epoch makes 1 + that × ceil(longest slice / batch)).
+ * Errors: PNN_ERR_INVALID.                                                  */
 pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches_per_epoch);
 
 /* Last error message of this handle (or of the last failed pnn_create when

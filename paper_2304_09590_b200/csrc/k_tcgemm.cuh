@@ -51,7 +51,24 @@ struct Epi {
     __nv_bfloat16* wbt;
     long long zs_w;
     float scale;
+    // z of blockIdx.z = 0 is zoff; when lr > 0 the update scale of tensor z is lr / bsz(z),
+    // bsz(z) = the rows of CN (zoff + z)'s slice in mini-batch `step` (short last batch, R14)
+    int zoff;
+    float lr;
+    long long n_local;
+    int K_local, step, batch;
 };
+
+__device__ __forceinline__ float update_scale(const Epi& ep, int z) {
+    if (ep.lr <= 0.f) return ep.scale;
+    long long st, cnt;
+    const long long base = ep.n_local / ep.K_local, rem = ep.n_local % ep.K_local;
+    cnt = base + ((z < rem) ? 1 : 0);
+    (void)st;
+    long long b = cnt - (long long)ep.step * ep.batch;
+    b = b < 0 ? 0 : (b > ep.batch ? ep.batch : b);
+    return b > 0 ? ep.lr / (float)b : 0.f;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
@@ -136,7 +153,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     GemmSmem<BN>& s = *reinterpret_cast<GemmSmem<BN>*>(
         raw + ((1024 - (smem_u32(raw) & 1023)) & 1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, z = blockIdx.z;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, z = blockIdx.z + ep.zoff;
     const int nk = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
@@ -224,12 +241,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
             }
         } else {  // EPI_UPD
+            const float scale = update_scale(ep, z);
             float* ms = ep.master + (long long)z * ep.zs_master + (long long)m * ep.N + nb;
             __nv_bfloat16* wb = ep.wb + (long long)z * ep.zs_w + (long long)m * ep.N + nb;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 if (nb + i < ep.nvalid) {
-                    const float w = fmaf(-ep.scale, v[i], ms[i]);   // W -= η·(Σ/B)
+                    const float w = fmaf(-scale, v[i], ms[i]);   // W -= η·(Σ/B)
                     ms[i] = w;
                     const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
                     wb[i] = w16;
@@ -239,7 +257,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
     }
     if constexpr (EPI == EPI_BWD) {
-        if (mok) ep.bias_upd[(long long)z * ep.zs_bias + m] -= ep.scale * rowsum;   // b -= η·(Σδ/B)
+        if (mok) ep.bias_upd[(long long)z * ep.zs_bias + m] -= update_scale(ep, z) * rowsum;   // b -= η·(Σδ/B)
     }
     fence_before();
     __syncthreads();

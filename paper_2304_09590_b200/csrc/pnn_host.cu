@@ -30,6 +30,7 @@ struct pnn_net_s {
     float* d_merged = nullptr;        // [P]
     double* d_msum = nullptr;         // [P] fp64 partial sums (multi-rank merge)
     float* d_gscratch = nullptr;      // [K_local][P] mini-batch gradient sums (lazy)
+    MbState* mb = nullptr;            // bf16 mini-batch buffers + tensor maps (lazy, a10)
     float4* d_gram = nullptr;         // [gram_rows] Gram terms of the resident kernel (lazy)
     long long gram_rows = 0;
     float* d_xstage = nullptr;        // host-input staging (lazy)
@@ -142,6 +143,7 @@ bool load_nccl(std::string& why) {
 }
 
 pnn_status alloc_local(pnn_net net) {
+    mb_destroy(net->mb); net->mb = nullptr;
     cudaFree(net->d_children); net->d_children = nullptr;
     cudaFree(net->d_gscratch); net->d_gscratch = nullptr;
     const size_t bytes = sizeof(float) * (size_t)net->d.P * (size_t)(net->K_local > 0 ? net->K_local : 1);
@@ -153,6 +155,7 @@ pnn_status alloc_local(pnn_net net) {
 }
 
 int choose_kernel(pnn_net net, ResidentPlan* plan) {
+    if (net->precision == PNN_BF16) return PNN_KERNEL_TC_BF16;
     if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
     *plan = plan_resident(net->d, net->batch);
     if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
@@ -165,7 +168,16 @@ pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long
     int k = choose_kernel(net, &plan);
     if (k < 0) return fail(net, PNN_ERR_INVALID, "resident kernel not valid here: %s", plan.why);
     cudaError_t e;
-    if (k == PNN_KERNEL_RESIDENT) {
+    if (k == PNN_KERNEL_TC_BF16) {
+        if (!net->mb) {
+            net->mb = mb_create(net->d, net->K_local, net->batch, &e);
+            if (!net->mb)
+                return fail(net, e == cudaErrorMemoryAllocation ? PNN_ERR_OOM : PNN_ERR_CUDA,
+                            "bf16 mini-batch buffers / tensor maps: %s", cudaGetErrorString(e));
+        }
+        e = launch_minibatch_bf16(net->mb, net->d, net->d_children, x, y, n, net->K_local, s_first,
+                                  s_count, net->lr, st);
+    } else if (k == PNN_KERNEL_RESIDENT) {
         if (net->gram_rows < n) {
             cudaFree(net->d_gram);
             net->d_gram = nullptr;
@@ -300,8 +312,11 @@ pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision) {
     if (batch < 1) return fail(net, PNN_ERR_INVALID, "batch = %d < 1", batch);
     if (precision != PNN_FP32 && precision != PNN_BF16)
         return fail(net, PNN_ERR_INVALID, "precision = %d unknown", precision);
-    if (precision == PNN_BF16)
-        return fail(net, PNN_ERR_INVALID, "PNN_BF16 mini-batch variant is not built yet");
+    if (precision == PNN_BF16) {
+        if (const char* why = mb_plan(net->d, batch))
+            return fail(net, PNN_ERR_INVALID, "PNN_BF16 mini-batch: %s", why);
+    }
+    if (precision != net->precision || batch != net->batch) { mb_destroy(net->mb); net->mb = nullptr; }
     net->batch = batch;
     net->precision = precision;
     return PNN_OK;
@@ -466,7 +481,8 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     ResidentPlan plan{};
     int k = choose_kernel(net, &plan);
     *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
-    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : 1;   // resident: Gram terms + training
+    // resident: Gram terms + training; tc bf16: weight cast + 8 per mini-batch step
+    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 8 : 1;
     return PNN_OK;
 }
 
@@ -483,6 +499,7 @@ pnn_status pnn_destroy(pnn_net net) {
     cudaFree(net->d_merged);
     cudaFree(net->d_msum);
     cudaFree(net->d_gscratch);
+    mb_destroy(net->mb);
     cudaFree(net->d_gram);
     cudaFree(net->d_xstage);
     cudaFree(net->d_ystage);

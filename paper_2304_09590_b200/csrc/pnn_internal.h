@@ -58,6 +58,16 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 int K_local, int s_first, int s_count, float lr,
                                 cudaStream_t st);
 
+// bf16 mini-batch variant on tcgen05 GEMMs (k_minibatch.cu): nullptr when the shape /
+// batch is supported, else the reason.
+struct MbState;
+const char* mb_plan(const NetDesc& d, int batch);
+MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err);
+void mb_destroy(MbState* s);
+cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children, const float* x,
+                                  const int32_t* y, long long n_local, int K_local, int s_first,
+                                  int s_count, float lr, cudaStream_t st);
+
 // Merge: sum[i] = Σ_{c<K_local} children[c][i] in fp64, ascending c.
 cudaError_t launch_merge_sum(const float* children, int K_local, long long P, double* sum,
                              cudaStream_t st);

@@ -22,7 +22,7 @@ STATUS_NAMES = ["PNN_OK", "PNN_ERR_INVALID", "PNN_ERR_SHAPE", "PNN_ERR_DATA", "P
 PNN_SIGMOID, PNN_TANH, PNN_RELU, PNN_SOFTMAX = 0, 1, 2, 3
 PNN_INIT_NORMAL, PNN_INIT_UNIFORM, PNN_INIT_XAVIER_NORMAL, PNN_INIT_HE_NORMAL = 0, 1, 2, 3
 PNN_FP32, PNN_BF16 = 0, 1
-PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT = 0, 1, 2
+PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16 = 0, 1, 2, 3
 ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX}
 INIT = {"normal": PNN_INIT_NORMAL, "uniform": PNN_INIT_UNIFORM, "xavier": PNN_INIT_XAVIER_NORMAL,
         "he": PNN_INIT_HE_NORMAL}
