@@ -108,19 +108,25 @@ def _oracle_sample(cfg, budget_s):
     S = int(count[0])
     per_cn = S * cfg.epochs * fma_per_sample(cfg.layers) * 2 / 1.0e9      # GFLOP per CN
     n_cn = int(max(1, min(cfg.K, budget_s * 1.2 * cores / per_cn)))
+    if n_cn * per_cn > budget_s * 1.2 * cores:       # whole CNs overrun: one CN per core, fewer rows
+        n_cn = min(cfg.K, cores)
+        per_row = cfg.epochs * fma_per_sample(cfg.layers) * 2 / 1.0e9
+        S = min(S, max(cfg.batch, int(budget_s * 1.2 / per_row) // cfg.batch * cfg.batch))
     if n_cn >= cores:
         n_cn = (n_cn // cores) * cores
     sample = list(range(n_cn))
     data = {int(start[i]): make_rows(int(start[i]), int(count[i]), "train", 0) for i in sample}
+    if S < int(count[0]):                             # truncated slices (train on the first S rows)
+        data = {k: (v[0][:S], v[1][:S]) for k, v in data.items()}
     threads = min(cores, n_cn)
 
     def run():
         oracle.train_pnn_rows(cfg.layers, cfg.act, cfg.init, cfg.K, cfg.lr, 0, cfg.n_train,
                               lambda s, c: data[s], epochs=cfg.epochs, batch=cfg.batch,
-                              threads=threads, subnets=sample)
+                              threads=threads, subnets=sample, precision=cfg.precision)
 
     desc = (f"{n_cn} of {cfg.K} CNs x {S} rows x {cfg.epochs} epoch(s), batch {cfg.batch}: "
-            f"fp32 oracle, one CN per thread, {threads} threads; merge/readout not timed")
+            f"{cfg.precision} oracle, one CN per thread, {threads} threads; merge/readout not timed")
     return run, n_cn * S * cfg.epochs, threads, desc
 
 
@@ -138,7 +144,8 @@ def run_reference(args, cfg):
     return {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if cfg.precision == "fp32" else "bf16-emulated f32",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": cfg.name, "layers": list(cfg.layers), "K": cfg.K,
                    "rows": cfg.n_train, "epochs": cfg.epochs, "batch": cfg.batch},
@@ -182,7 +189,7 @@ def main():
     import torch
     import torch.distributed as dist
     from datagen import make_rows
-    from paper_2304_09590_b200 import PNN
+    from paper_2304_09590_b200 import PNN, PNN_BF16
     from paper_2304_09590_b200.dist import nccl_unique_id_bytes, rank_rows, rank_subnets
 
     torch.cuda.set_device(local_rank)
@@ -196,7 +203,7 @@ def main():
     net = PNN(cfg.layers, cfg.act, cfg.init, cfg.K, cfg.lr, seed=0)
     net.set_kernel(args.kernel)
     if cfg.batch > 1:
-        net.set_minibatch(cfg.batch)
+        net.set_minibatch(cfg.batch, PNN_BF16 if cfg.precision == "bf16" else 0)
     if world > 1:
         net.set_comm(world, rank, nccl_unique_id_bytes(rank))
     kernel_id, launches_per_epoch = net.kernel_info()
@@ -283,30 +290,48 @@ def main():
         flop_launch = 2.0 * fma_per_sample(cfg.layers) * (nrows)   # this rank's launch
         achieved = flop_launch / (train_ms / 1e3) / 1e12
         peak_max = sms * 128 * 2 * (pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        if cfg.precision == "bf16":
+            peak_tc = pk.get("bf16_tflops_sustained", 1392.3)
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
+                    "frac": achieved / peak_tc, "traffic": None,
+                    "kernel": "training epoch (bf16 mini-batch: weight cast + 8 launches per step)",
+                    "peak_note": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS 8192^3 back to back); "
+                                 "flop = 2 x (3P - P1) per sample, of which the 10-wide output layer "
+                                 "(0.6%) runs on CUDA cores",
+                    "train_ms_per_launch": train_ms, "flop_per_launch": flop_launch}
+        else:
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak_max,
+                    "unit": "TFLOP/s", "frac": achieved / peak_max, "traffic": None,
+                    "kernel": "training epoch (Gram-term launch + persistent SGD launch)",
+                    "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
+                                 f"{pk.get('sm_max_mhz', 1965.0):.0f} MHz (guide unit counts, "
+                                 f"sm_max clock); at the measured {sm_mhz:.0f} MHz the frac "
+                                 f"is {achieved / (peak_max * sm_mhz / pk.get('sm_max_mhz', 1965.0)):.3f}",
+                    "train_ms_per_launch": train_ms,
+                    "flop_per_launch": flop_launch}
+        if cfg.precision == "bf16":
+            import math
+            steps_epoch = math.ceil(math.ceil(nrows / K_local) / cfg.batch)
+            launches_epoch = 1 + launches_per_epoch * steps_epoch
+        else:
+            launches_epoch = launches_per_epoch
         out = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16" if cfg.precision == "bf16" else "f32",
             "data": "synthetic (seeded MNIST-shaped stand-in, datagen/)",
             "config": {"workload": f"{cfg.name}: {'-'.join(map(str, cfg.layers))} "
                                    f"{'/'.join(cfg.act)}, {cfg.init} init, K={cfg.K} CNs, "
                                    f"{cfg.n_train} rows, {cfg.epochs} epoch(s), batch {cfg.batch}, "
                                    f"lr {cfg.lr}",
                        "K_local": K_local, "rows_per_rank": nrows, "test_rows": cfg.n_test,
-                       "kernel": ["auto", "reference", "resident"][kernel_id],
+                       "kernel": ["auto", "reference", "resident", "tc_bf16"][kernel_id],
                        "l2": f"inputs {X.nbytes / 2**20:.0f} MiB per rank > 126 MB L2 (no flush)"},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_max,
-                         "unit": "TFLOP/s", "frac": achieved / peak_max, "traffic": None,
-                         "kernel": "training epoch (Gram-term launch + persistent SGD launch)",
-                         "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
-                                      f"{pk.get('sm_max_mhz', 1965.0):.0f} MHz (guide unit counts, "
-                                      f"sm_max clock); at the measured {sm_mhz:.0f} MHz the frac "
-                                      f"is {achieved / (peak_max * sm_mhz / pk.get('sm_max_mhz', 1965.0)):.3f}",
-                         "train_ms_per_launch": train_ms,
-                         "flop_per_launch": flop_launch},
+            "roofline": roof,
             "breakdown_ms": {"train": train_ms * cfg.epochs, "merge_predict": ms - train_ms * cfg.epochs},
             "clocks": clocks,
-            "gpu_launches": args.steps * (cfg.epochs * launches_per_epoch + 2),
+            "gpu_launches": args.steps * (cfg.epochs * launches_epoch + 2),
         }
         if e2e:
             out["e2e"] = e2e

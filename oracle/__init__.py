@@ -249,9 +249,10 @@ def train_pnn(layers, act, init, K, lr, seed, X, y, epochs=1, batch=1, dtype=np.
 
 
 def train_pnn_rows(layers, act, init, K, lr, seed, N, rows, epochs=1, batch=1,
-                   dtype=np.float32, threads=1, subnets=None):
+                   dtype=np.float32, threads=1, subnets=None, precision="fp32"):
     p0 = init_params(layers, init, seed)
-    return _train_children(layers, act, p0, K, lr, N, rows, epochs, batch, dtype, threads, subnets)
+    return _train_children(layers, act, p0, K, lr, N, rows, epochs, batch, dtype, threads, subnets,
+                           precision)
 
 
 def _train_children(layers, act, p0, K, lr, N, rows, epochs, batch, dtype, threads, subnets,

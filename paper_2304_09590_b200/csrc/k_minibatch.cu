@@ -47,8 +47,16 @@ static cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int
                                const tc::Epi& ep, cudaStream_t st) {
     auto kern = tc::gemm_kernel<BN, EPI>;
     const size_t smem = tc::smem_bytes<BN>();
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static bool attr_done = false;                     // per instantiation (prepare_gemm_attrs sets the
+    if (!attr_done) {                                  // step's ones before any capture)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        if (cs == cudaStreamCaptureStatusNone) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            attr_done = true;
+        }
+    }
     dim3 grid((unsigned)((M + tc::BM - 1) / tc::BM), (unsigned)((N + BN - 1) / BN), (unsigned)Z);
     kern<<<grid, 128, smem, st>>>(ta, tb, K, ep);
     return cudaGetLastError();
@@ -89,7 +97,7 @@ extern "C" int pnn_debug_tc_gemm(const void* A, const void* B, float* C, int Z, 
 //   out_fwd  z3 = A2·W3bᵀ + b3, softmax, δ3 = p - e (0 past the batch), δ3b; b3 update
 //   out_bwd  dW3 = δ3bᵀ·A2 -> W3, W3b; dA2 = δ3b·W3b(old); δ2 = dA2 ⊙ [A2 > 0] -> δ2b,
 //            δ2bT; b2 update
-//   B4 (tc)  dA1ᵀ = W2bT·δ2bᵀ (pre-update W2, R6); δ1 = dA1 ⊙ [A1 > 0] -> δ1T; b1 update
+//   B4 (tc)  dA1ᵀ = W2bT·δ2bᵀ (pre-update W2, R6); δ1 = dA1 ⊙ [A1T > 0] -> δ1T; b1 update
 //   B3 (tc)  dW2 = δ2bT·A1Tᵀ -> W2 -= η/B·dW2, W2b, W2bT
 //   B5 (tc)  dW1 = δ1T·XsTᵀ  -> W1 -= η/B·dW1, W1b
 // =====================================================================================
@@ -100,7 +108,32 @@ struct MbState {
     __nv_bfloat16 *W1b, *W2b, *W2bT, *W3b, *Xs, *XsT, *A1, *A1T, *A2, *d2b, *d2bT, *d1T, *d3b;
     float* d3;
     CUtensorMap tW1b, tXs, tW2b, tA1, tW2bT, td2b, td2bT, tA1T, td1T, tXsT;
+    // the epoch's launch sequence as a CUDA graph, re-used while its arguments are unchanged
+    // (a small cache: the host-input path trains the CNs in a few groups)
+    cudaStream_t cap = nullptr;
+    struct G {
+        cudaGraphExec_t exec = nullptr;
+        const void *children = nullptr, *x = nullptr, *y = nullptr;
+        long long n = -1;
+        int first = -1, count = -1;
+        float lr = 0.f;
+        unsigned long long used = 0;
+    } g[8];
+    unsigned long long tick = 0;
 };
+
+// dynamic shared-memory opt-in of the GEMM instantiations the step uses (before any capture)
+static cudaError_t prepare_gemm_attrs() {
+    cudaError_t e = cudaFuncSetAttribute(tc::gemm_kernel<64, tc::EPI_FWD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::smem_bytes<64>());
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc::gemm_kernel<64, tc::EPI_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tc::smem_bytes<64>());
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc::gemm_kernel<256, tc::EPI_UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tc::smem_bytes<256>());
+    return e;
+}
 
 const char* mb_plan(const NetDesc& d, int batch) {
     if (d.L != 3) return "bf16 mini-batch is built for 3-layer nets (D-H1-H2-O)";
@@ -120,6 +153,9 @@ void mb_destroy(MbState* s) {
                              s->d2bT, s->d1T, s->d3b};
     for (auto* b : bufs) cudaFree(b);
     cudaFree(s->d3);
+    for (auto& e : s->g)
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (s->cap) cudaStreamDestroy(s->cap);
     delete s;
 }
 
@@ -138,7 +174,9 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     for (auto& a : al)
         if (*err == cudaSuccess) *err = cudaMalloc(a.p, sizeof(__nv_bfloat16) * (size_t)a.n);
     if (*err == cudaSuccess) *err = cudaMalloc(&s->d3, sizeof(float) * (size_t)(Z * B * 16));
-    if (*err == cudaSuccess) cudaMemset(s->W3b, 0, sizeof(__nv_bfloat16) * (size_t)(Z * 16 * H2));
+    if (*err == cudaSuccess) *err = cudaMemset(s->W3b, 0, sizeof(__nv_bfloat16) * (size_t)(Z * 16 * H2));
+    if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
+    if (*err == cudaSuccess) *err = prepare_gemm_attrs();
     bool ok = *err == cudaSuccess;
     const int iZ = (int)Z;
     ok = ok && make_tmap_kmajor(&s->tW1b, s->W1b, (int)D, (int)H1, iZ, tc::BM);
@@ -195,92 +233,99 @@ __global__ void mb_cast_w(const float* __restrict__ children, MbState s, int z0,
     }
 }
 
-// Xs[z][b][d] = bf16(x[row]) and XsT[z][d][b], row = start(z) + step·B + b (0 past the slice)
-__global__ void mb_cast_x(const float* __restrict__ X, MbState s, long long n_local, int K_local, int z0, int step) {
-    const int z = z0 + blockIdx.y;
+// Xs[z][b][d] = bf16(x[row]) and XsT[z][d][b], row = start(z) + step·B + b (0 past the
+// slice); one CTA per 64-column chunk of d and CN, transposed through shared memory so
+// that both stores are coalesced.
+__global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, MbState s, long long n_local,
+                                                 int K_local, int z0, int step) {
+    __shared__ __nv_bfloat16 t[64][66];
+    const int z = z0 + blockIdx.y, d0 = blockIdx.x * 64;
     long long st;
     const long long cnt = slice_rows(n_local, K_local, z, &st);
-    const int b = blockIdx.x;                      // one CTA per batch row
-    const long long t = (long long)step * s.B + b;
-    const bool live = t < cnt;
-    const float* xr = X + (st + t) * s.D;
-    for (int dcol = threadIdx.x; dcol < s.D; dcol += blockDim.x) {
-        const __nv_bfloat16 v = __float2bfloat16_rn(live ? xr[dcol] : 0.f);
-        s.Xs[((long long)z * s.B + b) * s.D + dcol] = v;
-        s.XsT[((long long)z * s.D + dcol) * s.B + b] = v;
+    const int w = (s.D - d0) < 64 ? (s.D - d0) : 64;
+    for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+        const int b = idx >> 6, dd = idx & 63;
+        const long long tr = (long long)step * s.B + b;
+        if (b < s.B && dd < w) {
+            const __nv_bfloat16 v = __float2bfloat16_rn(tr < cnt ? X[(st + tr) * s.D + d0 + dd] : 0.f);
+            s.Xs[((long long)z * s.B + b) * s.D + d0 + dd] = v;
+            t[b][dd] = v;
+        }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+        const int dd = idx >> 6, b = idx & 63;
+        if (b < s.B && dd < w) s.XsT[((long long)z * s.D + d0 + dd) * s.B + b] = t[b][dd];
     }
 }
 
-// Output layer forward + δ3 (one CTA of 8 warps per CN; warp w: batch rows w, w+8, ...)
-__global__ void __launch_bounds__(256) mb_out_fwd(float* __restrict__ children, const int32_t* __restrict__ Y,
-                                                  MbState s, long long n_local, int K_local, int z0, int step,
-                                                  float lr) {
-    extern __shared__ float w3s[];                 // [O][H2] fp32 copy of W3b
-    __shared__ float dsum[16][8];
-    const int z = z0 + blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Output layer forward + δ3: one warp per batch row (grid: B/8 × CNs, 8 warps); z3 = A2·W3bᵀ
+// + b3 with the bf16 operands in fp32, softmax (max-subtracted, R4), δ3 = p − e (Eq.10),
+// 0 for rows past the slice (short last batch, R14).
+__global__ void __launch_bounds__(256) mb_out_fwd(const float* __restrict__ children, const int32_t* __restrict__ Y,
+                                                  MbState s, long long n_local, int K_local, int z0, int step) {
+    const int z = z0 + blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * 8 + warp;
     long long st;
     const long long cnt = slice_rows(n_local, K_local, z, &st);
     long long bsz = cnt - (long long)step * s.B;
     bsz = bsz < 0 ? 0 : (bsz > s.B ? s.B : bsz);
-    float* P = children + (long long)z * s.P;
-    const float* b3 = P + s.woff3 + (long long)s.O * s.H2;
-    for (int i = threadIdx.x; i < s.O * s.H2; i += blockDim.x)
-        w3s[i] = __bfloat162float(s.W3b[(long long)z * 16 * s.H2 + i]);
-    __syncthreads();
-    float dacc[16];
+    const float* b3 = children + (long long)z * s.P + s.woff3 + (long long)s.O * s.H2;
+    const __nv_bfloat16* a2 = s.A2 + ((long long)z * s.B + b) * s.H2;
+    const __nv_bfloat16* w3 = s.W3b + (long long)z * 16 * s.H2;
+    float acc[16];
 #pragma unroll
-    for (int o = 0; o < 16; ++o) dacc[o] = 0.f;
-    for (int b = warp; b < s.B; b += 8) {
-        const __nv_bfloat16* a2 = s.A2 + ((long long)z * s.B + b) * s.H2;
-        float acc[16];
+    for (int o = 0; o < 16; ++o) acc[o] = 0.f;
+    for (int j = 8 * lane; j < s.H2; j += 256) {
+        const uint4 av = *reinterpret_cast<const uint4*>(a2 + j);
+        const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&av);
+        float a[8];
 #pragma unroll
-        for (int o = 0; o < 16; ++o) acc[o] = 0.f;
-        for (int j = lane; j < s.H2; j += 32) {
-            const float a = __bfloat162float(a2[j]);
-#pragma unroll
-            for (int o = 0; o < 16; ++o)
-                if (o < s.O) acc[o] = fmaf(a, w3s[o * s.H2 + j], acc[o]);
-        }
-#pragma unroll
-        for (int o = 0; o < 16; ++o)
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], off);
-        // softmax (max-subtracted, R4) and δ3 = p - e (Eq.10); rows past the slice: 0
-        float m = -INFINITY;
-#pragma unroll
-        for (int o = 0; o < 16; ++o)
-            if (o < s.O) { acc[o] += b3[o]; m = fmaxf(m, acc[o]); }
-        float sum = 0.f;
-#pragma unroll
-        for (int o = 0; o < 16; ++o)
-            if (o < s.O) { acc[o] = expf(acc[o] - m); sum += acc[o]; }
-        const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;
+        for (int q = 0; q < 4; ++q) { const float2 f = __bfloat1622float2(ap[q]); a[2 * q] = f.x; a[2 * q + 1] = f.y; }
 #pragma unroll
         for (int o = 0; o < 16; ++o) {
-            float dl = 0.f;
-            if (o < s.O && b < bsz) dl = acc[o] / sum - ((o == label) ? 1.f : 0.f);
-            dacc[o] += dl;
-            if (lane == o) {
-                s.d3[((long long)z * s.B + b) * 16 + o] = dl;
-                s.d3b[((long long)z * s.B + b) * 16 + o] = __float2bfloat16_rn(dl);
+            if (o < s.O) {
+                const uint4 wv = *reinterpret_cast<const uint4*>(w3 + (long long)o * s.H2 + j);
+                const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&wv);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(wp[q]);
+                    acc[o] = fmaf(a[2 * q], f.x, acc[o]);
+                    acc[o] = fmaf(a[2 * q + 1], f.y, acc[o]);
+                }
             }
         }
     }
-    if (lane == 0)
 #pragma unroll
-        for (int o = 0; o < 16; ++o) dsum[o][warp] = dacc[o];
-    __syncthreads();
-    if (threadIdx.x < s.O && bsz > 0) {            // b3 -= η·(Σ_b δ3 / B)
-        float t = 0.f;
-        for (int w = 0; w < 8; ++w) t += dsum[threadIdx.x][w];
-        P[s.woff3 + (long long)s.O * s.H2 + threadIdx.x] -= (lr / (float)bsz) * t;
+    for (int o = 0; o < 16; ++o)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], off);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int o = 0; o < 16; ++o)
+        if (o < s.O) { acc[o] += b3[o]; mx = fmaxf(mx, acc[o]); }
+    float sum = 0.f;
+#pragma unroll
+    for (int o = 0; o < 16; ++o)
+        if (o < s.O) { acc[o] = expf(acc[o] - mx); sum += acc[o]; }
+    const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+        if (lane == o) {
+            const float dl = (o < s.O && b < bsz) ? acc[o] / sum - ((o == label) ? 1.f : 0.f) : 0.f;
+            s.d3[((long long)z * s.B + b) * 16 + o] = dl;
+            s.d3b[((long long)z * s.B + b) * 16 + o] = __float2bfloat16_rn(dl);
+        }
     }
 }
 
-// Output layer backward, one thread per hidden unit j of layer 2
-__global__ void __launch_bounds__(128) mb_out_bwd(float* __restrict__ children, MbState s, long long n_local,
+// Output layer backward (grid: H2/64 × CNs, 256 threads = 64 hidden units × 4 batch
+// quarters): dW3 = δ3bᵀ·A2 → W3, W3b; dA2 = δ3b·W3b (pre-update W3, R6); δ2 = dA2 ⊙
+// [A2 > 0] (R9) → δ2b [B][H2] and δ2bT [H2][B]; b2 -= η·Σδ2/B; block 0 also b3 -= η·Σδ3/B.
+__global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, MbState s, long long n_local,
                                                   int K_local, int z0, int step, float lr) {
     __shared__ float d3s[64][16];
+    __shared__ float part[3][64][17];
     const int z = z0 + blockIdx.y;
     long long st;
     const long long cnt = slice_rows(n_local, K_local, z, &st);
@@ -290,11 +335,14 @@ __global__ void __launch_bounds__(128) mb_out_bwd(float* __restrict__ children, 
     for (int i = threadIdx.x; i < s.B * 16; i += blockDim.x)
         (&d3s[0][0])[i] = __bfloat162float(s.d3b[(long long)z * s.B * 16 + i]);
     __syncthreads();
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= s.H2) return;
     float* P = children + (long long)z * s.P;
-    float* W3 = P + s.woff3;
-    float* b2 = P + s.woff2 + (long long)s.H2 * s.H1;
+    if (blockIdx.x == 0 && threadIdx.x < s.O) {        // b3 -= η·(Σ_b δ3 / B), δ3 in fp32
+        float t = 0.f;
+        for (int b = 0; b < s.B; ++b) t += s.d3[((long long)z * s.B + b) * 16 + threadIdx.x];
+        P[s.woff3 + (long long)s.O * s.H2 + threadIdx.x] -= scale * t;
+    }
+    const int jl = threadIdx.x & 63, g = threadIdx.x >> 6;
+    const int j = blockIdx.x * 64 + jl;
     __nv_bfloat16* w3b = s.W3b + (long long)z * 16 * s.H2;
     float wold[16], gw[16];
 #pragma unroll
@@ -305,49 +353,65 @@ __global__ void __launch_bounds__(128) mb_out_bwd(float* __restrict__ children, 
     float db = 0.f;
     const __nv_bfloat16* a2 = s.A2 + (long long)z * s.B * s.H2 + j;
     __nv_bfloat16* d2b = s.d2b + (long long)z * s.B * s.H2 + j;
-    __nv_bfloat16* d2bT = s.d2bT + ((long long)z * s.H2 + j) * s.B;
-    for (int b = 0; b < s.B; ++b) {
-        const float a = __bfloat162float(a2[(long long)b * s.H2]);
-        float da = 0.f;                            // (W3bᵀ δ3b)_j with the pre-update W3 (R6)
+    uint4* d2bT = reinterpret_cast<uint4*>(s.d2bT + ((long long)z * s.H2 + j) * s.B + 16 * g);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        __align__(16) __nv_bfloat16 pk[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int b = 16 * g + 8 * h + q;
+            const float a = __bfloat162float(a2[(long long)b * s.H2]);
+            float da = 0.f;
+#pragma unroll
+            for (int o = 0; o < 16; ++o) {
+                if (o < s.O) {
+                    gw[o] = fmaf(d3s[b][o], a, gw[o]);
+                    da = fmaf(wold[o], d3s[b][o], da);
+                }
+            }
+            const float d2 = (a > 0.f) ? da : 0.f;
+            pk[q] = __float2bfloat16_rn(d2);
+            d2b[(long long)b * s.H2] = pk[q];
+            db += d2;
+        }
+        d2bT[h] = *reinterpret_cast<const uint4*>(pk);
+    }
+    if (g > 0) {
+#pragma unroll
+        for (int o = 0; o < 16; ++o) part[g - 1][jl][o] = gw[o];
+        part[g - 1][jl][16] = db;
+    }
+    __syncthreads();
+    if (g == 0) {
+        for (int q = 0; q < 3; ++q) {
+#pragma unroll
+            for (int o = 0; o < 16; ++o) gw[o] += part[q][jl][o];
+            db += part[q][jl][16];
+        }
+        float* W3 = P + s.woff3;
 #pragma unroll
         for (int o = 0; o < 16; ++o) {
             if (o < s.O) {
-                gw[o] = fmaf(d3s[b][o], a, gw[o]);             // dW3[o][j] = Σ_b δ3b·A2
-                da = fmaf(wold[o], d3s[b][o], da);
+                const float w = fmaf(-scale, gw[o], W3[(long long)o * s.H2 + j]);
+                W3[(long long)o * s.H2 + j] = w;
+                w3b[(long long)o * s.H2 + j] = __float2bfloat16_rn(w);
             }
         }
-        const float d2 = (a > 0.f) ? da : 0.f;                 // ⊙ ReLU'(z2) (R9)
-        const __nv_bfloat16 d2h = __float2bfloat16_rn(d2);
-        d2b[(long long)b * s.H2] = d2h;
-        d2bT[b] = d2h;
-        db += d2;
+        P[s.woff2 + (long long)s.H2 * s.H1 + j] -= scale * db;
     }
-#pragma unroll
-    for (int o = 0; o < 16; ++o) {
-        if (o < s.O) {
-            const float w = fmaf(-scale, gw[o], W3[(long long)o * s.H2 + j]);
-            W3[(long long)o * s.H2 + j] = w;
-            w3b[(long long)o * s.H2 + j] = __float2bfloat16_rn(w);
-        }
-    }
-    b2[j] -= scale * db;
 }
 
 }  // namespace
 
-cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children, const float* x,
-                                  const int32_t* y, long long n_local, int K_local, int s_first, int s_count,
-                                  float lr, cudaStream_t st) {
-    if (s_count <= 0) return cudaSuccess;
+static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, const int32_t* y,
+                                 long long n_local, int K_local, int s_first, int s_count, float lr,
+                                 cudaStream_t st) {
     const int B = s->B;
     long long st0, cnt0;
     shard_of(n_local, K_local, s_first, &st0, &cnt0);
     const long long steps = (cnt0 + B - 1) / B;    // the first slice is the longest (R17)
     mb_cast_w<<<1184, 256, 0, st>>>(children, *s, s_first, s_count);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    const size_t out_smem = sizeof(float) * (size_t)s->O * s->H2;
-    e = cudaFuncSetAttribute(mb_out_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out_smem);
     if (e != cudaSuccess) return e;
     tc::Epi base{};
     base.zoff = s_first;
@@ -357,7 +421,8 @@ cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children,
     base.batch = B;
     for (long long j = 0; j < steps; ++j) {
         base.step = (int)j;
-        mb_cast_x<<<dim3((unsigned)B, (unsigned)s_count), 256, 0, st>>>(x, *s, n_local, K_local, s_first, (int)j);
+        mb_cast_x<<<dim3((unsigned)((s->D + 63) / 64), (unsigned)s_count), 256, 0, st>>>(x, *s, n_local, K_local,
+                                                                                      s_first, (int)j);
         // F1: A1 = relu(W1b·Xsᵀ + b1)
         tc::Epi f1 = base;
         f1.M = s->H1; f1.N = B; f1.nvalid = B;
@@ -371,13 +436,14 @@ cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children,
         f2.out_bm = s->A2; f2.out_mb = nullptr; f2.zs_act = (long long)s->H2 * B;
         if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW2b, s->tA1, s_count, s->H2, B, s->H1, f2, st))) return e;
         // output layer (CUDA cores: N = 10 / K = 10 are not dense contractions)
-        mb_out_fwd<<<s_count, 256, out_smem, st>>>(children, y, *s, n_local, K_local, s_first, (int)j, lr);
-        mb_out_bwd<<<dim3((unsigned)((s->H2 + 127) / 128), (unsigned)s_count), 128, 0, st>>>(
+        mb_out_fwd<<<dim3((unsigned)(B / 8), (unsigned)s_count), 256, 0, st>>>(children, y, *s, n_local, K_local,
+                                                                                 s_first, (int)j);
+        mb_out_bwd<<<dim3((unsigned)(s->H2 / 64), (unsigned)s_count), 256, 0, st>>>(
             children, *s, n_local, K_local, s_first, (int)j, lr);
         // B4: δ1 = (W2bᵀ·δ2b) ⊙ [A1 > 0]; b1 update (pre-update W2: before B3)
         tc::Epi b4 = base;
         b4.M = s->H1; b4.N = B; b4.nvalid = B;
-        b4.mask = s->A1; b4.out_mb = s->d1T; b4.zs_act = (long long)s->H1 * B;
+        b4.mask = s->A1T; b4.out_mb = s->d1T; b4.zs_act = (long long)s->H1 * B;
         b4.bias_upd = children + s->woff1 + (long long)s->H1 * s->D; b4.zs_bias = s->P;
         if ((e = launch_gemm<64, tc::EPI_BWD>(s->tW2bT, s->td2b, s_count, s->H1, B, s->H2, b4, st))) return e;
         // B3: W2 -= η/B · δ2bᵀ·A1
@@ -394,4 +460,39 @@ cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children,
         if ((e = launch_gemm<256, tc::EPI_UPD>(s->td1T, s->tXsT, s_count, s->H1, s->D, B, b5, st))) return e;
     }
     return cudaGetLastError();
+}
+
+// One epoch = 1 + 8·steps launches; captured once into a CUDA graph (keyed by every
+// argument the launches bake in) and replayed, so the host issues one launch per epoch.
+cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children, const float* x,
+                                  const int32_t* y, long long n_local, int K_local, int s_first, int s_count,
+                                  float lr, cudaStream_t st) {
+    (void)d;
+    if (s_count <= 0) return cudaSuccess;
+    MbState::G* hit = nullptr;
+    MbState::G* lru = &s->g[0];
+    for (auto& e : s->g) {
+        if (e.exec && e.children == children && e.x == x && e.y == y && e.n == n_local && e.first == s_first &&
+            e.count == s_count && e.lr == lr)
+            hit = &e;
+        if (e.used < lru->used) lru = &e;
+    }
+    if (!hit) {
+        hit = lru;
+        if (hit->exec) { cudaGraphExecDestroy(hit->exec); hit->exec = nullptr; }
+        cudaError_t e = cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return e;
+        cudaError_t eq = enqueue_epoch(s, children, x, y, n_local, K_local, s_first, s_count, lr, s->cap);
+        cudaGraph_t g = nullptr;
+        e = cudaStreamEndCapture(s->cap, &g);
+        if (eq != cudaSuccess) { if (g) cudaGraphDestroy(g); return eq; }
+        if (e != cudaSuccess) return e;
+        e = cudaGraphInstantiate(&hit->exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) { hit->exec = nullptr; return e; }
+        hit->children = children; hit->x = x; hit->y = y; hit->n = n_local;
+        hit->first = s_first; hit->count = s_count; hit->lr = lr;
+    }
+    hit->used = ++s->tick;
+    return cudaGraphLaunch(hit->exec, st);
 }

@@ -23,7 +23,9 @@ using namespace ptx;
 
 constexpr int BM = 128;       // tile rows (UMMA M)
 constexpr int BK = 64;        // K per stage: 64 bf16 = one 128-byte swizzle row
-constexpr int STAGES = 4;
+// pipeline depth: 8 stages for the narrow tiles (long K: more TMA loads in flight), 2 for BN = 256 (the update GEMMs
+// have K = 64, a single stage) so that two CTAs fit per SM
+__host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? 2 : 8; }
 
 enum { EPI_STORE_F32 = 0, EPI_FWD = 1, EPI_BWD = 2, EPI_UPD = 3 };
 
@@ -40,7 +42,7 @@ struct Epi {
     __nv_bfloat16* out_bm;
     __nv_bfloat16* out_mb;
     long long zs_act;         // M·N elements per z for both activation layouts
-    // EPI_BWD: d = acc ⊙ [mask[z][n][m] > 0]; out_mb[z][m][n] = bf16(d);
+    // EPI_BWD: d = acc ⊙ [mask[z][m][n] > 0]; out_mb[z][m][n] = bf16(d);
     //          bias[m] -= scale · Σ_{n < nvalid} d  (the layer's bias update)
     const __nv_bfloat16* mask;
     float* bias_upd;
@@ -116,6 +118,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes × 32 consecutive 32-bit TMEM columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // Shared-memory matrix descriptor of a K-major tile written by TMA with the 128-byte swizzle:
 // rows of 128 bytes, 8-row core groups 1024 bytes apart (SBO), LBO unused, version 1
 // (sm_100), layout type 2 = SWIZZLE_128B.  Advancing along K inside the swizzle atom adds
@@ -140,6 +158,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
 
 template <int BN>
 struct __align__(1024) GemmSmem {
+    static constexpr int STAGES = stages_for(BN);
     __nv_bfloat16 a[STAGES][BM * BK];     // 16 KB per stage
     __nv_bfloat16 b[STAGES][BN * BK];
     uint64_t full[STAGES], empty[STAGES], accf;
@@ -147,7 +166,7 @@ struct __align__(1024) GemmSmem {
 };
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, Epi ep) {
     extern __shared__ __align__(1024) unsigned char raw[];
     GemmSmem<BN>& s = *reinterpret_cast<GemmSmem<BN>*>(
@@ -155,6 +174,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, z = blockIdx.z + ep.zoff;
     const int nk = (K + BK - 1) / BK;
+    constexpr int STAGES = GemmSmem<BN>::STAGES;
+    static_assert(sizeof(GemmSmem<BN>::a) >= 4 * 32 * 33 * sizeof(float), "epilogue tile");
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
@@ -197,67 +218,110 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         mma_commit(&s.accf);                           // accumulator complete
     }
     // ---------------- epilogue: all 4 warps ----------------
+    // Per 32-column chunk: (1) lane = tile row (the TMEM lane layout): per-row work and the
+    // [n][m] outputs, which are coalesced in this mapping; (2) through a padded shared tile,
+    // lane = column: the [m][n] outputs, coalesced 128-byte rows.  The operand stages are
+    // free once the accumulator is complete, so the transpose tile reuses them.
     __syncwarp();
     mbar_wait(&s.accf, 0u);
     __syncwarp();
     fence_after();
-    const int m = m0 + 32 * warp + lane;               // this thread's tile row
+    float (*tile)[33] = reinterpret_cast<float (*)[33]>(&s.a[0][0]) + 32 * warp;
+    const int mrow0 = m0 + 32 * warp;
+    const int m = mrow0 + lane;                        // phase-1 row of this thread
     const bool mok = m < ep.M;
     float rowsum = 0.f;
+    float scale = 0.f;
+    if constexpr (EPI == EPI_UPD || EPI == EPI_BWD) scale = update_scale(ep, z);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c, v);
+    for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c, v);
         const int nb = n0 + c;
-        if (!mok) continue;
-        if constexpr (EPI == EPI_STORE_F32) {
-            float* o = ep.out_f32 + (long long)z * ep.zs_out + (long long)m * ep.N + nb;
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-                if (nb + i < ep.nvalid) o[i] = v[i];
-        } else if constexpr (EPI == EPI_FWD) {
-            const float b = ep.bias[(long long)z * ep.zs_bias + m];
+        // ---- phase 1: lane = row
+        if constexpr (EPI == EPI_FWD) {
+            const float b = mok ? ep.bias[(long long)z * ep.zs_bias + m] : 0.f;
             __nv_bfloat16* obm = ep.out_bm + (long long)z * ep.zs_act;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float y = fmaxf(v[i] + b, 0.f);    // φ = ReLU (Eq.4), bias once (R1)
-                const __nv_bfloat16 yb = __float2bfloat16_rn(y);
-                if (nb + i < ep.nvalid) {
-                    obm[(long long)(nb + i) * ep.M + m] = yb;
-                    if (ep.out_mb) ep.out_mb[(long long)z * ep.zs_act + (long long)m * ep.N + nb + i] = yb;
-                }
-            }
-        } else if constexpr (EPI == EPI_BWD) {
-            const __nv_bfloat16* mk = ep.mask + (long long)z * ep.zs_act;
-            __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + (long long)m * ep.N;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (nb + i < ep.nvalid) {
-                    const float d = (__bfloat162float(mk[(long long)(nb + i) * ep.M + m]) > 0.f) ? v[i] : 0.f;
-                    omb[nb + i] = __float2bfloat16_rn(d);
-                    rowsum += d;
-                } else if (nb + i < ep.N) {
-                    omb[nb + i] = __float2bfloat16_rn(0.f);
-                }
-            }
-        } else {  // EPI_UPD
-            const float scale = update_scale(ep, z);
-            float* ms = ep.master + (long long)z * ep.zs_master + (long long)m * ep.N + nb;
-            __nv_bfloat16* wb = ep.wb + (long long)z * ep.zs_w + (long long)m * ep.N + nb;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                if (nb + i < ep.nvalid) {
-                    const float w = fmaf(-scale, v[i], ms[i]);   // W -= η·(Σ/B)
-                    ms[i] = w;
-                    const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
-                    wb[i] = w16;
-                    if (ep.wbt) ep.wbt[(long long)z * ep.zs_w + (long long)(nb + i) * ep.M + m] = w16;
-                }
+            for (int i = 0; i < 32; ++i) {
+                const __nv_bfloat16 yb = __float2bfloat16_rn(fmaxf(v[i] + b, 0.f));   // ReLU (Eq.4), bias once (R1)
+                if (mok && nb + i < ep.nvalid) obm[(long long)(nb + i) * ep.M + m] = yb;
+                v[i] = __bfloat162float(yb);
             }
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tile[lane][i] = v[i];
+        __syncwarp();
+        // ---- phase 2: lane = column n = nb + lane
+        const int n = nb + lane;
+        const bool nok = n < ep.nvalid;
+        if constexpr (EPI == EPI_STORE_F32) {
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r)
+                if (mrow0 + r < ep.M && nok)
+                    ep.out_f32[(long long)z * ep.zs_out + (long long)(mrow0 + r) * ep.N + n] = tile[r][lane];
+        } else if constexpr (EPI == EPI_FWD) {
+            if (ep.out_mb) {
+                __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + n;
+#pragma unroll 4
+                for (int r = 0; r < 32; ++r)
+                    if (mrow0 + r < ep.M && nok) omb[(long long)(mrow0 + r) * ep.N] = __float2bfloat16_rn(tile[r][lane]);
+            }
+        } else if constexpr (EPI == EPI_BWD) {
+            // d = acc ⊙ [mask > 0] (ReLU'(z) from the stored activation, R9), mask [m][n]
+            const __nv_bfloat16* mk = ep.mask + (long long)z * ep.zs_act + n;
+            __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + n;
+            const int rows = (ep.M - mrow0) < 32 ? (ep.M - mrow0) : 32;
+            __nv_bfloat16 mv[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r)
+                mv[r] = (r < rows && nok) ? mk[(long long)(mrow0 + r) * ep.N] : __float2bfloat16_rn(0.f);
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                const float d = (__bfloat162float(mv[r]) > 0.f) ? tile[r][lane] : 0.f;
+                tile[r][lane] = d;
+                if (r < rows && n < ep.N) omb[(long long)(mrow0 + r) * ep.N] = __float2bfloat16_rn(d);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rowsum += tile[lane][i];     // phase 3: lane = row
+        } else {  // EPI_UPD: W -= η·(Σ/B), bf16 copy
+            float* ms = ep.master + (long long)z * ep.zs_master + n;
+            __nv_bfloat16* wb = ep.wb + (long long)z * ep.zs_w + n;
+            const int rows = (ep.M - mrow0) < 32 ? (ep.M - mrow0) : 32;
+            if (nok && rows == 32) {
+                float old[32];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) old[r] = ms[(long long)(mrow0 + r) * ep.N];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) {
+                    const float w = fmaf(-scale, tile[r][lane], old[r]);
+                    ms[(long long)(mrow0 + r) * ep.N] = w;
+                    const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
+                    wb[(long long)(mrow0 + r) * ep.N] = w16;
+                    tile[r][lane] = __bfloat162float(w16);
+                }
+            } else if (nok) {
+                for (int r = 0; r < rows; ++r) {
+                    const float w = fmaf(-scale, tile[r][lane], ms[(long long)(mrow0 + r) * ep.N]);
+                    ms[(long long)(mrow0 + r) * ep.N] = w;
+                    const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
+                    wb[(long long)(mrow0 + r) * ep.N] = w16;
+                    tile[r][lane] = __bfloat162float(w16);
+                }
+            }
+            if (ep.wbt) {                              // ---- phase 3: lane = row again, [n][m] copy
+                __syncwarp();
+                __nv_bfloat16* wt = ep.wbt + (long long)z * ep.zs_w + m;
+#pragma unroll 4
+                for (int i = 0; i < 32; ++i)
+                    if (mok && nb + i < ep.nvalid) wt[(long long)(nb + i) * ep.M] = __float2bfloat16_rn(tile[lane][i]);
+            }
+        }
+        __syncwarp();
     }
     if constexpr (EPI == EPI_BWD) {
-        if (mok) ep.bias_upd[(long long)z * ep.zs_bias + m] -= update_scale(ep, z) * rowsum;   // b -= η·(Σδ/B)
+        if (mok) ep.bias_upd[(long long)z * ep.zs_bias + m] -= scale * rowsum;   // b -= η·(Σδ/B)
     }
     fence_before();
     __syncthreads();

@@ -83,3 +83,29 @@ def test_bf16_rejects_unsupported_shapes():
     net = PNN([784, 1024, 1024, 10], ["relu", "relu", "softmax"], "he", 2, 0.01, seed=0)
     with pytest.raises(PnnError, match="batch 64"):
         net.set_minibatch(32, PNN_BF16)
+
+
+def test_bf16_deterministic_and_host_path_identical():
+    """Two device-input runs and one host-input run (pinned buffers, CN groups staged
+    while earlier groups train) give bit-identical CNs; the second epoch replays the
+    cached CUDA graph of the first."""
+    from paper_2304_09590_b200 import PNN
+    from paper_2304_09590_b200.pnn import PNN_BF16
+    c = CONFIGS["C5"]
+    K, n = 4, 4 * 100 + 3
+    X, y = make_split(n, "train", 0)
+
+    def run(host):
+        net = PNN(c.layers, c.act, c.init, K, c.lr, seed=0)
+        net.set_minibatch(64, PNN_BF16)
+        for _ in range(2):
+            if host:
+                net.train_epoch_host(torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory())
+            else:
+                net.train_epoch(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+        torch.cuda.synchronize()
+        return np.stack([net.get_params(i) for i in range(K)])
+
+    a, b, h = run(False), run(False), run(True)
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(a, h)

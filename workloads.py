@@ -17,6 +17,7 @@ class Config:
     n_test: int
     epochs: int = 1
     batch: int = 1
+    precision: str = "fp32"
     note: str = ""
 
 
@@ -32,8 +33,8 @@ CONFIGS = {
     # configs[3]: 784-128-10 ReLU/softmax, He-normal, K=1024 (128/GPU × 8), η=0.01, 2^20 rows
     "C4": Config("C4", (784, 128, 10), ("relu", "softmax"), "he", 1024, 0.01, 1 << 20, 10000),
     # configs[4]: 784-1024-1024-10 ReLU (R13: softmax+CE output), K=8, mini-batch 64, η=0.05,
-    # 480k rows, 3 epochs; bf16 tcgen05 variant (a10) — fp32 mini-batch until it lands
+    # 480k rows, 3 epochs; bf16 operands / fp32 accumulate + master (R25) on tcgen05 (a10)
     "C5": Config("C5", (784, 1024, 1024, 10), ("relu", "relu", "softmax"), "he", 8, 0.05,
-                 480000, 10000, epochs=3, batch=64,
+                 480000, 10000, epochs=3, batch=64, precision="bf16",
                  note="init unstated; He-normal (ReLU)"),
 }
