@@ -302,17 +302,22 @@ def main():
         else:
             roof = {"bound": "alu", "achieved": achieved, "peak": peak_max,
                     "unit": "TFLOP/s", "frac": achieved / peak_max, "traffic": None,
-                    "kernel": "training epoch (Gram-term launch + persistent SGD launch)",
+                    "kernel": {1: "training epoch (reference kernel)",
+                               2: "training epoch (Gram-term launch + persistent SGD launch)",
+                               4: "training epoch (fp32 mini-batch: 4 launches per step, CUDA graph)"}
+                              .get(kernel_id, "training epoch"),
                     "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
                                  f"{pk.get('sm_max_mhz', 1965.0):.0f} MHz (guide unit counts, "
                                  f"sm_max clock); at the measured {sm_mhz:.0f} MHz the frac "
                                  f"is {achieved / (peak_max * sm_mhz / pk.get('sm_max_mhz', 1965.0)):.3f}",
                     "train_ms_per_launch": train_ms,
                     "flop_per_launch": flop_launch}
-        if cfg.precision == "bf16":
-            import math
-            steps_epoch = math.ceil(math.ceil(nrows / K_local) / cfg.batch)
+        import math
+        steps_epoch = math.ceil(math.ceil(nrows / K_local) / cfg.batch)
+        if kernel_id == 3:          # bf16 tcgen05 mini-batch: weight cast + 8 per step
             launches_epoch = 1 + launches_per_epoch * steps_epoch
+        elif kernel_id == 4:        # fp32 mini-batch step kernels: 4 per step
+            launches_epoch = launches_per_epoch * steps_epoch
         else:
             launches_epoch = launches_per_epoch
         out = {
@@ -326,7 +331,7 @@ def main():
                                    f"{cfg.n_train} rows, {cfg.epochs} epoch(s), batch {cfg.batch}, "
                                    f"lr {cfg.lr}",
                        "K_local": K_local, "rows_per_rank": nrows, "test_rows": cfg.n_test,
-                       "kernel": ["auto", "reference", "resident", "tc_bf16"][kernel_id],
+                       "kernel": ["auto", "reference", "resident", "tc_bf16", "mb_f32"][kernel_id],
                        "l2": f"inputs {X.nbytes / 2**20:.0f} MiB per rank > 126 MB L2 (no flush)"},
             "roofline": roof,
             "breakdown_ms": {"train": train_ms * cfg.epochs, "merge_predict": ms - train_ms * cfg.epochs},

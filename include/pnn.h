@@ -61,7 +61,9 @@ typedef enum {
  * (Eq.6; δ^L = x - e, Eq.10); any other output → C = ½Σ(x - e)² (reading
  * R11; δ^L = (x - e)⊙φ'(z^L), Eq.9).  PNN_SOFTMAX is only valid on the last
  * layer.                                                                    */
-enum { PNN_SIGMOID = 0, PNN_TANH = 1, PNN_RELU = 2, PNN_SOFTMAX = 3 };
+enum { PNN_SIGMOID = 0, PNN_TANH = 1, PNN_RELU = 2, PNN_SOFTMAX = 3,
+       PNN_LEAKY_RELU = 4   /* φ(z) = z ≥ 0 ? z : 0.01·z (PAPER.md:281 names it, §5.2;
+                               slope unstated → 0.01, DESIGN.md §3 R28)          */ };
 
 /* Initialisation (reading R15).  Weights / biases:
  *   NORMAL         N(0,1) / N(0,1)          (the paper's NormFloat64)
@@ -80,9 +82,12 @@ enum { PNN_FP32 = 0, PNN_BF16 = 1 };
 enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          */
        PNN_KERNEL_REFERENCE = 1, /* one CTA per CN, weights in global memory    */
        PNN_KERNEL_RESIDENT = 2,  /* persistent cluster kernel, on-chip weights  */
-       PNN_KERNEL_TC_BF16 = 3    /* bf16 mini-batch on tcgen05 GEMMs; chosen by
+       PNN_KERNEL_TC_BF16 = 3,   /* bf16 mini-batch on tcgen05 GEMMs; chosen by
                                     pnn_set_minibatch(.., PNN_BF16), reported
-                                    by pnn_kernel_info, not settable         */ };
+                                    by pnn_kernel_info, not settable         */
+       PNN_KERNEL_MB_F32 = 4     /* fp32 mini-batch step kernels (D-H-O nets,
+                                    batch 2..64; AUTO picks it, REFERENCE
+                                    opts out), reported, not settable        */ };
 
 /* Build a PNN of n_subnets CNs with layer sizes layers[0..n_layers-1]
  * (layers[0] = inputs, e.g. {784,128,10}; n_layers >= 2, each size >= 1,
@@ -126,6 +131,14 @@ pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision);
  * PNN_ERR_INVALID when the shape does not fit it.        */
 pnn_status pnn_set_kernel(pnn_net net, int32_t kernel);
 
+/* Limit how many local CNs train concurrently (the GPU
+ * analogue of the paper's goroutine count, Table 2): each
+ * pnn_train_epoch then trains the CNs in consecutive waves of `slots` CNs, one
+ * wave after the other on the stream.  0 (the default) = all local CNs in one
+ * wave.  Results are identical for every slots value (the CNs are independent).
+ * Errors: PNN_ERR_INVALID (slots < 0).                                       */
+pnn_status pnn_set_slots(pnn_net net, int32_t slots);
+
 /* One training epoch of every local CN ("Each child-network
  * learns only a slice of the dataset"; :225-231).  x: device fp32
  * [n][layers[0]] row-major; labels: device int32 [n], each in
@@ -163,6 +176,23 @@ pnn_status pnn_merge(pnn_net net, void* cuda_stream);
 pnn_status pnn_predict(pnn_net net, int32_t subnet, const float* x, int64_t n,
                        int32_t* labels_out, void* cuda_stream);
 
+/* Evaluation metrics of the merged network (subnet = -1) or a local CN (global
+ * index) on n labelled rows (x: device fp32 [n][layers[0]], labels: device int32
+ * [n]), the quantities of the paper's experiments (PAPER.md
+ * :333-401, 486-547), computed in fp64 from the fp32 parameters (as pnn_predict):
+ *   metrics_out[0] accuracy   = fraction of rows whose readout label (argmax z^L,
+ *                               ties → lowest, R19) equals the label;
+ *   metrics_out[1] confidence = mean over rows of max_k x^L_k (softmax output: the
+ *                               predicted class's probability; the paper never
+ *                               defines confidence — reading R29);
+ *   metrics_out[2] cost       = mean over rows of −log(max(x^L_y, 1e-12)) (Eq.6,
+ *                               PAPER.md:100-103, ε-clamp R29).
+ * A label outside [0, n_out) counts as wrong with the ε cost.  Synchronises
+ * cuda_stream (metrics_out is host memory).  Errors: PNN_ERR_INVALID (NULL
+ * pointer, n <= 0, subnet not local), PNN_ERR_OOM, PNN_ERR_CUDA.             */
+pnn_status pnn_evaluate(pnn_net net, int32_t subnet, const float* x, const int32_t* labels, int64_t n,
+                        double* metrics_out, void* cuda_stream);
+
 /* Copy parameters to host_out (n_floats must equal P_total).  subnet = -1:
  * the merged network; otherwise a local CN (global index).  Synchronises
  * the device.  Errors: PNN_ERR_INVALID, PNN_ERR_SHAPE, PNN_ERR_CUDA.        */
@@ -186,7 +216,8 @@ pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count);
 
 /* Which training kernel the next pnn_train_epoch launches (PNN_KERNEL_*),
  * and how many kernel launches it makes (PNN_KERNEL_TC_BF16: launches per
- * mini-batch step; an epoch makes 1 + that × ceil(longest slice / batch)).
+ * mini-batch step; an epoch makes 1 + that × ceil(longest slice / batch);
+ * PNN_KERNEL_MB_F32: per step, an epoch makes that × ceil(longest slice / batch)).
  * Errors: PNN_ERR_INVALID.                                                  */
 pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches_per_epoch);
 

@@ -30,9 +30,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
-SIGMOID, TANH, RELU, SOFTMAX = 0, 1, 2, 3
+SIGMOID, TANH, RELU, SOFTMAX, LEAKY_RELU = 0, 1, 2, 3, 4
 INIT_NORMAL, INIT_UNIFORM, INIT_XAVIER, INIT_HE = 0, 1, 2, 3
-ACT_NAMES = {"sigmoid": SIGMOID, "tanh": TANH, "relu": RELU, "softmax": SOFTMAX}
+ACT_NAMES = {"sigmoid": SIGMOID, "tanh": TANH, "relu": RELU, "softmax": SOFTMAX, "leaky_relu": LEAKY_RELU}
 INIT_NAMES = {"normal": INIT_NORMAL, "uniform": INIT_UNIFORM, "xavier": INIT_XAVIER, "he": INIT_HE}
 
 _lib = None
@@ -214,6 +214,38 @@ def predict(layers, act, params, X, dtype=np.float64, return_logits=False):
     getattr(lib(), "orc_predict" + suf)(_p(layers), L, _p(act), _p(params), _p(X), n,
                                        _p(labels), _p(logits) if logits is not None else None)
     return (labels, logits) if return_logits else labels
+
+
+def evaluate(layers, act, params, X, y):
+    """f2 evaluation metrics of one network on labelled rows, in fp64:
+
+    * accuracy   = fraction of rows whose readout label (predict, R19) equals y;
+    * confidence = mean over rows of max_k x^L_k, x^L the output activation (softmax:
+      the predicted class's probability; undefined in the paper, reading R29);
+    * cost       = mean over rows of −log(max(x^L_y, 1e-12)) (Eq.6, PAPER.md:100-103:
+      C = −Σ_i e_i log x_i with one-hot e; ε-clamp R29).
+    x^L from the fp64 logits z^L: softmax exp(z − max z)/Σ (Eq.5 with R4), else φ_L(z)
+    (sigmoid 1/(1+e^−z), tanh, ReLU, leaky ReLU (R28) as in Eqs.3-4)."""
+    layers_, act_, L = _net(layers, act)
+    labels, z = predict(layers, act, params, X, return_logits=True)
+    a = int(act_[-1])
+    if a == SOFTMAX:
+        e = np.exp(z - z.max(axis=1, keepdims=True))
+        x = e / e.sum(axis=1, keepdims=True)
+    elif a == SIGMOID:
+        x = 1.0 / (1.0 + np.exp(-z))
+    elif a == TANH:
+        x = np.tanh(z)
+    elif a == RELU:
+        x = np.where(z >= 0, z, 0.0)
+    else:
+        x = np.where(z >= 0, z, float(np.float32(0.01)) * z)
+    y = np.asarray(y, dtype=np.int64)
+    rows = np.arange(len(y))
+    acc = float(np.mean(labels == y))
+    conf = float(np.mean(x.max(axis=1)))
+    cost = float(np.mean(-np.log(np.maximum(x[rows, y], 1e-12))))
+    return acc, conf, cost
 
 
 def shard_bounds(N: int, K: int):

@@ -26,7 +26,7 @@
 #include <string.h>
 
 #define ORC_MAX_LAYERS 16
-enum { ORC_SIGMOID = 0, ORC_TANH = 1, ORC_RELU = 2, ORC_SOFTMAX = 3 };
+enum { ORC_SIGMOID = 0, ORC_TANH = 1, ORC_RELU = 2, ORC_SOFTMAX = 3, ORC_LEAKY_RELU = 4 };
 enum { ORC_INIT_NORMAL = 0, ORC_INIT_UNIFORM = 1, ORC_INIT_XAVIER = 2, ORC_INIT_HE = 3 };
 
 /* ---- fp32 instantiation ------------------------------------------------ */

@@ -17,9 +17,15 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTile = 8;
 
+// EVAL: also the per-row evaluation terms of f2: the output
+// activation x^L (softmax max-subtracted, R4, or φ_L), its maximum (confidence,
+// reading R29) and the cross-entropy term −log(max(x^L_y, 1e-12)) (Eq.6, PAPER.md:100-103;
+// ε-clamp R29), plus whether the readout label equals y.
+template <bool EVAL>
 __global__ void __launch_bounds__(kThreads)
 predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restrict__ X,
-               long long n, int32_t* __restrict__ labels) {
+               long long n, int32_t* __restrict__ labels, const int32_t* __restrict__ ytrue,
+               double* __restrict__ rowstats) {
     extern __shared__ double smd[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = d.max_width;
@@ -64,20 +70,54 @@ predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restr
             const double* z = in + tid * W;
             int best = 0;
             for (int k = 1; k < d.n[d.L]; ++k) if (z[k] > z[best]) best = k;
-            labels[t0 + tid] = best;
+            if (labels) labels[t0 + tid] = best;
+            if constexpr (EVAL) {
+                const int O = d.n[d.L], a = d.act[d.L - 1], yv = ytrue[t0 + tid];
+                double xmax, xy;
+                if (a == PNN_SOFTMAX) {
+                    double sum = 0.0;
+                    for (int k = 0; k < O; ++k) sum += exp(z[k] - z[best]);
+                    xmax = 1.0 / sum;
+                    xy = (yv >= 0 && yv < O) ? exp(z[yv] - z[best]) / sum : 0.0;
+                } else {
+                    xmax = -INFINITY;
+                    for (int k = 0; k < O; ++k) xmax = fmax(xmax, act_fwd_d(a, z[k]));
+                    xy = (yv >= 0 && yv < O) ? act_fwd_d(a, z[yv]) : 0.0;
+                }
+                double* r = rowstats + 3 * (t0 + tid);
+                r[0] = (best == yv) ? 1.0 : 0.0;
+                r[1] = xmax;
+                r[2] = -log(fmax(xy, 1e-12));
+            }
         }
         __syncthreads();
     }
 }
 
-}  // namespace
+// Mean of each of the 3 row-statistic columns over n rows: one CTA, fixed
+// per-thread strides and a fixed tree, so the result is deterministic.
+__global__ void __launch_bounds__(1024) eval_reduce(const double* __restrict__ rowstats, long long n,
+                                                    double* __restrict__ out) {
+    __shared__ double sh[3][1024];
+    double a[3] = {0.0, 0.0, 0.0};
+    for (long long i = threadIdx.x; i < n; i += 1024)
+        for (int c = 0; c < 3; ++c) a[c] += rowstats[3 * i + c];
+    for (int c = 0; c < 3; ++c) sh[c][threadIdx.x] = a[c];
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+            for (int c = 0; c < 3; ++c) sh[c][threadIdx.x] += sh[c][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 3) out[threadIdx.x] = sh[threadIdx.x][0] / (double)n;
+}
 
-cudaError_t launch_predict(const NetDesc& d, const float* params, const float* x, long long n,
-                           int32_t* labels, cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
+template <bool EVAL>
+cudaError_t launch_pred(const NetDesc& d, const float* params, const float* x, long long n, int32_t* labels,
+                        const int32_t* ytrue, double* rowstats, cudaStream_t st) {
     size_t smem = sizeof(double) * 2 * kTile * (size_t)d.max_width;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(predict_kernel,
+        cudaError_t e = cudaFuncSetAttribute(predict_kernel<EVAL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
@@ -86,6 +126,23 @@ cudaError_t launch_predict(const NetDesc& d, const float* params, const float* x
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     long long tiles = (n + kTile - 1) / kTile;
     int grid = (int)(tiles < (long long)sms * 4 ? tiles : (long long)sms * 4);
-    predict_kernel<<<grid, kThreads, smem, st>>>(d, params, x, n, labels);
+    predict_kernel<EVAL><<<grid, kThreads, smem, st>>>(d, params, x, n, labels, ytrue, rowstats);
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_evaluate(const NetDesc& d, const float* params, const float* x, const int32_t* y,
+                            long long n, double* rowstats, double* out3, cudaStream_t st) {
+    if (n <= 0) return cudaErrorInvalidValue;
+    cudaError_t e = launch_pred<true>(d, params, x, n, nullptr, y, rowstats, st);
+    if (e != cudaSuccess) return e;
+    eval_reduce<<<1, 1024, 0, st>>>(rowstats, n, out3);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const NetDesc& d, const float* params, const float* x, long long n,
+                           int32_t* labels, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    return launch_pred<false>(d, params, x, n, labels, nullptr, nullptr, st);
 }

@@ -702,6 +702,7 @@ cudaError_t launch_c(const ResidentPlan& p, const NetDesc& d, float* children, c
     PNN_ACTS(PNN_SIGMOID, PNN_SIGMOID)
     PNN_ACTS(PNN_TANH, PNN_TANH)
     PNN_ACTS(PNN_RELU, PNN_SIGMOID)
+    PNN_ACTS(PNN_LEAKY_RELU, PNN_SOFTMAX)
 #undef PNN_ACTS
     return cudaErrorInvalidValue;
 }
@@ -725,7 +726,8 @@ ResidentPlan plan_resident(const NetDesc& d, int batch) {
     const int a1 = d.act[0], a2 = d.act[1];
     const bool built = (a1 == PNN_RELU && a2 == PNN_SOFTMAX) || (a1 == PNN_TANH && a2 == PNN_SOFTMAX) ||
                        (a1 == PNN_SIGMOID && a2 == PNN_SOFTMAX) || (a1 == PNN_SIGMOID && a2 == PNN_SIGMOID) ||
-                       (a1 == PNN_TANH && a2 == PNN_TANH) || (a1 == PNN_RELU && a2 == PNN_SIGMOID);
+                       (a1 == PNN_TANH && a2 == PNN_TANH) || (a1 == PNN_RELU && a2 == PNN_SIGMOID) ||
+                       (a1 == PNN_LEAKY_RELU && a2 == PNN_SOFTMAX);
     if (!built) return no("activation pair not instantiated in the resident kernel");
     int c = 1;
     while (c <= CMAX && (H + c - 1) / c > UMAX) c *= 2;

@@ -25,7 +25,7 @@ constexpr int BM = 128;       // tile rows (UMMA M)
 constexpr int BK = 64;        // K per stage: 64 bf16 = one 128-byte swizzle row
 // pipeline depth: 8 stages for the narrow tiles (long K: more TMA loads in flight), 2 for BN = 256 (the update GEMMs
 // have K = 64, a single stage) so that two CTAs fit per SM
-__host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? 2 : 8; }
+__host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? 2 : (bn >= 128 ? 4 : 8); }
 
 enum { EPI_STORE_F32 = 0, EPI_FWD = 1, EPI_BWD = 2, EPI_UPD = 3 };
 

@@ -11,6 +11,7 @@ __device__ __forceinline__ float act_fwd(int act, float z) {
     case PNN_SIGMOID: return 1.f / (1.f + expf(-z));
     case PNN_TANH: return tanhf(z);
     case PNN_RELU: return z >= 0.f ? z : 0.f;      // Eq.4
+    case PNN_LEAKY_RELU: return z >= 0.f ? z : 0.01f * z;   // R28
     default: return z;
     }
 }
@@ -21,6 +22,7 @@ __device__ __forceinline__ float act_deriv_from_x(int act, float x) {
     case PNN_SIGMOID: return x * (1.f - x);
     case PNN_TANH: return 1.f - x * x;
     case PNN_RELU: return x > 0.f ? 1.f : 0.f;
+    case PNN_LEAKY_RELU: return x > 0.f ? 1.f : 0.01f;
     default: return 1.f;
     }
 }
@@ -30,6 +32,7 @@ __device__ __forceinline__ double act_fwd_d(int act, double z) {
     case PNN_SIGMOID: return 1.0 / (1.0 + exp(-z));
     case PNN_TANH: return tanh(z);
     case PNN_RELU: return z >= 0.0 ? z : 0.0;
+    case PNN_LEAKY_RELU: return z >= 0.0 ? z : (double)0.01f * z;   // fp32 slope, exact product
     default: return z;
     }
 }
@@ -72,11 +75,13 @@ template <int A> __device__ __forceinline__ float act_fwd_t(float z) {
     if constexpr (A == PNN_SIGMOID) return __frcp_rn(1.f + expf(-z));   // == 1.f/(1+e^-z), IEEE
     else if constexpr (A == PNN_TANH) return tanhf(z);
     else if constexpr (A == PNN_RELU) return z >= 0.f ? z : 0.f;
+    else if constexpr (A == PNN_LEAKY_RELU) return z >= 0.f ? z : 0.01f * z;
     else return z;
 }
 template <int A> __device__ __forceinline__ float act_deriv_t(float x) {
     if constexpr (A == PNN_SIGMOID) return x * (1.f - x);
     else if constexpr (A == PNN_TANH) return 1.f - x * x;
     else if constexpr (A == PNN_RELU) return x > 0.f ? 1.f : 0.f;
+    else if constexpr (A == PNN_LEAKY_RELU) return x > 0.f ? 1.f : 0.01f;
     else return 1.f;
 }

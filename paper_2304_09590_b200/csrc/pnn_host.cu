@@ -26,13 +26,17 @@ struct pnn_net_s {
     int k_first = 0, K_local = 1;     // this rank's CNs [k_first, k_first + K_local)
     void* comm = nullptr;             // ncclComm_t
     int batch = 1, precision = PNN_FP32, kernel = PNN_KERNEL_AUTO;
+    int slots = 0;                    // CNs trained concurrently (0 = all local CNs; f4)
     float* d_children = nullptr;      // [K_local][P]
     float* d_merged = nullptr;        // [P]
     double* d_msum = nullptr;         // [P] fp64 partial sums (multi-rank merge)
     float* d_gscratch = nullptr;      // [K_local][P] mini-batch gradient sums (lazy)
     MbState* mb = nullptr;            // bf16 mini-batch buffers + tensor maps (lazy, a10)
+    Mb32State* mb32 = nullptr;        // fp32 mini-batch buffers (lazy, f1)
     float4* d_gram = nullptr;         // [gram_rows] Gram terms of the resident kernel (lazy)
     long long gram_rows = 0;
+    double* d_eval = nullptr;         // evaluation row statistics [eval_rows][3] + 3 means (lazy)
+    long long eval_rows = 0;
     float* d_xstage = nullptr;        // host-input staging (lazy)
     int32_t* d_ystage = nullptr;
     long long stage_rows = 0;
@@ -144,6 +148,7 @@ bool load_nccl(std::string& why) {
 
 pnn_status alloc_local(pnn_net net) {
     mb_destroy(net->mb); net->mb = nullptr;
+    mb32_destroy(net->mb32); net->mb32 = nullptr;
     cudaFree(net->d_children); net->d_children = nullptr;
     cudaFree(net->d_gscratch); net->d_gscratch = nullptr;
     const size_t bytes = sizeof(float) * (size_t)net->d.P * (size_t)(net->K_local > 0 ? net->K_local : 1);
@@ -156,14 +161,32 @@ pnn_status alloc_local(pnn_net net) {
 
 int choose_kernel(pnn_net net, ResidentPlan* plan) {
     if (net->precision == PNN_BF16) return PNN_KERNEL_TC_BF16;
+    if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1 && !mb32_plan(net->d, net->batch))
+        return PNN_KERNEL_MB_F32;
     if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
     *plan = plan_resident(net->d, net->batch);
     if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
     return plan->ok ? PNN_KERNEL_RESIDENT : PNN_KERNEL_REFERENCE;
 }
 
+pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long long n,
+                             int s_first, int s_count, cudaStream_t st);
+
+// Train local CNs [s_first, s_first + s_count), in waves of at most `slots` CNs (f4: the
+// GPU analogue of the paper's goroutine count) when a limit is set.
 pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long n,
                         int s_first, int s_count, cudaStream_t st) {
+    const int w = (net->slots > 0 && net->slots < s_count) ? net->slots : s_count;
+    for (int s0 = s_first; s0 < s_first + s_count; s0 += w) {
+        const int c = (s_first + s_count - s0) < w ? (s_first + s_count - s0) : w;
+        pnn_status r = launch_train_wave(net, x, y, n, s0, c, st);
+        if (r != PNN_OK) return r;
+    }
+    return PNN_OK;
+}
+
+pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long long n,
+                             int s_first, int s_count, cudaStream_t st) {
     ResidentPlan plan{};
     int k = choose_kernel(net, &plan);
     if (k < 0) return fail(net, PNN_ERR_INVALID, "resident kernel not valid here: %s", plan.why);
@@ -177,6 +200,15 @@ pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long
         }
         e = launch_minibatch_bf16(net->mb, net->d, net->d_children, x, y, n, net->K_local, s_first,
                                   s_count, net->lr, st);
+    } else if (k == PNN_KERNEL_MB_F32) {
+        if (!net->mb32) {
+            net->mb32 = mb32_create(net->d, net->K_local, net->batch, &e);
+            if (!net->mb32)
+                return fail(net, e == cudaErrorMemoryAllocation ? PNN_ERR_OOM : PNN_ERR_CUDA,
+                            "fp32 mini-batch buffers: %s", cudaGetErrorString(e));
+        }
+        e = launch_minibatch_f32(net->mb32, net->d, net->d_children, x, y, n, net->K_local, s_first, s_count,
+                                 net->lr, st);
     } else if (k == PNN_KERNEL_RESIDENT) {
         if (net->gram_rows < n) {
             cudaFree(net->d_gram);
@@ -225,7 +257,7 @@ pnn_status pnn_create(const int32_t* layers, int32_t n_layers, const int32_t* ac
         for (int i = 0; i < n_layers; ++i)
             if (layers[i] <= 0) add("layers[" + std::to_string(i) + "] = " + std::to_string(layers[i]) + " <= 0");
         for (int i = 0; i < n_layers - 1; ++i) {
-            if (activation[i] < PNN_SIGMOID || activation[i] > PNN_SOFTMAX)
+            if (activation[i] < PNN_SIGMOID || activation[i] > PNN_LEAKY_RELU)
                 add("activation[" + std::to_string(i) + "] = " + std::to_string(activation[i]) + " unknown");
             else if (activation[i] == PNN_SOFTMAX && i != n_layers - 2)
                 add("softmax on hidden layer " + std::to_string(i + 1));
@@ -316,7 +348,10 @@ pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision) {
         if (const char* why = mb_plan(net->d, batch))
             return fail(net, PNN_ERR_INVALID, "PNN_BF16 mini-batch: %s", why);
     }
-    if (precision != net->precision || batch != net->batch) { mb_destroy(net->mb); net->mb = nullptr; }
+    if (precision != net->precision || batch != net->batch) {
+        mb_destroy(net->mb); net->mb = nullptr;
+        mb32_destroy(net->mb32); net->mb32 = nullptr;
+    }
     net->batch = batch;
     net->precision = precision;
     return PNN_OK;
@@ -332,6 +367,14 @@ pnn_status pnn_set_kernel(pnn_net net, int32_t kernel) {
         if (!p.ok) return fail(net, PNN_ERR_INVALID, "resident kernel not valid: %s", p.why);
     }
     net->kernel = kernel;
+    return PNN_OK;
+}
+
+pnn_status pnn_set_slots(pnn_net net, int32_t slots) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (slots < 0) return fail(net, PNN_ERR_INVALID, "slots = %d < 0", slots);
+    net->slots = slots;
     return PNN_OK;
 }
 
@@ -410,6 +453,34 @@ pnn_status pnn_merge(pnn_net net, void* stream) {
     return PNN_OK;
 }
 
+pnn_status pnn_evaluate(pnn_net net, int32_t subnet, const float* x, const int32_t* labels, int64_t n,
+                        double* metrics_out, void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!x || !labels || !metrics_out || n <= 0)
+        return fail(net, PNN_ERR_INVALID, "x/labels/metrics_out NULL or n <= 0");
+    const float* p;
+    if (subnet == -1) p = net->d_merged;
+    else if (subnet >= net->k_first && subnet < net->k_first + net->K_local)
+        p = net->d_children + (size_t)(subnet - net->k_first) * net->d.P;
+    else return fail(net, PNN_ERR_INVALID, "subnet %d is not local ([%d, %d))", subnet, net->k_first,
+                     net->k_first + net->K_local);
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    if (net->eval_rows < n) {
+        cudaFree(net->d_eval);
+        net->d_eval = nullptr;
+        net->eval_rows = 0;
+        CUDA_TRY(net, cudaMalloc(&net->d_eval, sizeof(double) * (3 * (size_t)n + 3)));
+        net->eval_rows = n;
+    }
+    double* out3 = net->d_eval + 3 * (size_t)net->eval_rows;
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(net, launch_evaluate(net->d, p, x, labels, n, net->d_eval, out3, s));
+    CUDA_TRY(net, cudaMemcpyAsync(metrics_out, out3, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(net, cudaStreamSynchronize(s));
+    return PNN_OK;
+}
+
 pnn_status pnn_predict(pnn_net net, int32_t subnet, const float* x, int64_t n, int32_t* labels,
                        void* stream) {
     pnn_status st = check_live(net);
@@ -482,7 +553,7 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     int k = choose_kernel(net, &plan);
     *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
     // resident: Gram terms + training; tc bf16: weight cast + 8 per mini-batch step
-    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 8 : 1;
+    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 8 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
     return PNN_OK;
 }
 
@@ -500,6 +571,8 @@ pnn_status pnn_destroy(pnn_net net) {
     cudaFree(net->d_msum);
     cudaFree(net->d_gscratch);
     mb_destroy(net->mb);
+    mb32_destroy(net->mb32);
+    cudaFree(net->d_eval);
     cudaFree(net->d_gram);
     cudaFree(net->d_xstage);
     cudaFree(net->d_ystage);

@@ -68,6 +68,15 @@ cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children,
                                   const int32_t* y, long long n_local, int K_local, int s_first,
                                   int s_count, float lr, cudaStream_t st);
 
+// fp32 mini-batch kernels for D-H-O nets (k_minibatch_f32.cu; f1): nullptr when supported.
+struct Mb32State;
+const char* mb32_plan(const NetDesc& d, int batch);
+Mb32State* mb32_create(const NetDesc& d, int K_local, int batch, cudaError_t* err);
+void mb32_destroy(Mb32State* s);
+cudaError_t launch_minibatch_f32(Mb32State* s, const NetDesc& d, float* children, const float* x,
+                                 const int32_t* y, long long n_local, int K_local, int s_first,
+                                 int s_count, float lr, cudaStream_t st);
+
 // Merge: sum[i] = Σ_{c<K_local} children[c][i] in fp64, ascending c.
 cudaError_t launch_merge_sum(const float* children, int K_local, long long P, double* sum,
                              cudaStream_t st);
@@ -79,5 +88,9 @@ cudaError_t launch_merge_local(const float* children, int K_local, long long P, 
                                float* merged, cudaStream_t st);
 
 // Predict: labels[i] = argmax z^L (fp64 forward from fp32 params), ties → lowest.
+// f2 evaluation: rowstats [n][3] scratch; out3 (device) = mean of (correct, max x^L,
+// −log max(x^L_y, 1e-12)) over the n rows.
+cudaError_t launch_evaluate(const NetDesc& d, const float* params, const float* x, const int32_t* y,
+                            long long n, double* rowstats, double* out3, cudaStream_t st);
 cudaError_t launch_predict(const NetDesc& d, const float* params, const float* x, long long n,
                            int32_t* labels, cudaStream_t st);

@@ -19,11 +19,13 @@ PNN_OK, PNN_ERR_INVALID, PNN_ERR_SHAPE, PNN_ERR_DATA, PNN_ERR_STATE, PNN_ERR_CUD
     PNN_ERR_NCCL, PNN_ERR_OOM = range(8)
 STATUS_NAMES = ["PNN_OK", "PNN_ERR_INVALID", "PNN_ERR_SHAPE", "PNN_ERR_DATA", "PNN_ERR_STATE",
                 "PNN_ERR_CUDA", "PNN_ERR_NCCL", "PNN_ERR_OOM"]
-PNN_SIGMOID, PNN_TANH, PNN_RELU, PNN_SOFTMAX = 0, 1, 2, 3
+PNN_SIGMOID, PNN_TANH, PNN_RELU, PNN_SOFTMAX, PNN_LEAKY_RELU = 0, 1, 2, 3, 4
 PNN_INIT_NORMAL, PNN_INIT_UNIFORM, PNN_INIT_XAVIER_NORMAL, PNN_INIT_HE_NORMAL = 0, 1, 2, 3
 PNN_FP32, PNN_BF16 = 0, 1
-PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16 = 0, 1, 2, 3
-ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX}
+PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16, PNN_KERNEL_MB_F32 = \
+    0, 1, 2, 3, 4
+ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX,
+       "leaky_relu": PNN_LEAKY_RELU}
 INIT = {"normal": PNN_INIT_NORMAL, "uniform": PNN_INIT_UNIFORM, "xavier": PNN_INIT_XAVIER_NORMAL,
         "he": PNN_INIT_HE_NORMAL}
 KERNEL = {"auto": PNN_KERNEL_AUTO, "reference": PNN_KERNEL_REFERENCE, "resident": PNN_KERNEL_RESIDENT}
@@ -31,7 +33,7 @@ KERNEL = {"auto": PNN_KERNEL_AUTO, "reference": PNN_KERNEL_REFERENCE, "resident"
 EXPORTS = ["pnn_create", "pnn_set_comm", "pnn_set_minibatch", "pnn_set_kernel", "pnn_train_epoch",
            "pnn_train_epoch_host", "pnn_merge", "pnn_predict", "pnn_get_params", "pnn_set_params",
            "pnn_device_params", "pnn_param_count", "pnn_local_subnets", "pnn_kernel_info",
-           "pnn_last_error", "pnn_destroy"]
+           "pnn_last_error", "pnn_destroy", "pnn_evaluate", "pnn_set_slots"]
 
 _lib = None
 
@@ -72,6 +74,8 @@ def load(path: str | None = None):
         "pnn_kernel_info": ([V, P32, P32], I32),
         "pnn_last_error": ([V], ctypes.c_char_p),
         "pnn_destroy": ([V], I32),
+        "pnn_evaluate": ([V, I32, V, V, I64, V, V], I32),
+        "pnn_set_slots": ([V, I32], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -174,6 +178,19 @@ class PNN:
         self._check(self._L.pnn_predict(self.h, int(subnet), _ptr(x, torch.float32), x.shape[0],
                                         _ptr(labels_out, torch.int32), ctypes.c_void_p(_stream_ptr(stream))))
         return labels_out
+
+    def evaluate(self, x, labels, subnet=-1, stream=None):
+        """(accuracy, confidence, cost) of the merged net (-1) or a local CN on
+        labelled device rows (pnn_evaluate; fp64; synchronises the stream)."""
+        import torch
+        out = np.zeros(3, dtype=np.float64)
+        self._check(self._L.pnn_evaluate(self.h, int(subnet), _ptr(x, torch.float32), _ptr(labels, torch.int32),
+                                         x.shape[0], out.ctypes.data_as(ctypes.c_void_p),
+                                         ctypes.c_void_p(_stream_ptr(stream))))
+        return tuple(float(v) for v in out)
+
+    def set_slots(self, slots):
+        self._check(self._L.pnn_set_slots(self.h, int(slots)))
 
     def get_params(self, subnet=-1) -> np.ndarray:
         out = np.empty(self.param_count, dtype=np.float32)

@@ -45,7 +45,7 @@ KERNELS = ["reference", "auto"]
 
 
 def _train(cfg_layers, act, init, K, lr, X, y, epochs=1, kernel="auto", batch=1):
-    net = PNN(cfg_layers, act, init, K, lr, seed=0, kernel="reference" if batch > 1 else kernel)
+    net = PNN(cfg_layers, act, init, K, lr, seed=0, kernel=kernel)
     if batch > 1:
         net.set_minibatch(batch)
     xd, yd = dev(X), dev(y)
@@ -112,6 +112,64 @@ def test_reduced_configs(orc, name, K, n, epochs, kernel):
     np.testing.assert_array_equal(lab0, orc.predict(c.layers, c.act, kids[0], Xt))
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_leaky_relu_c4_shape(orc, kernel):
+    """f3: leaky ReLU hidden layer (slope 0.01, R28) on the C4 shape,
+    reference and resident kernels vs the oracle."""
+    c = CONFIGS["C4"]
+    act = ["leaky_relu", "softmax"]
+    K, n = 32, 32 * 80 + 11
+    X, y = make_split(n, "train", 0)
+    Xt, _ = make_split(500, "test", 0)
+    net, kids, merged = _train(c.layers, act, c.init, K, c.lr, X, y, 1, kernel)
+    if kernel == "auto":
+        assert net.kernel_info()[0] == 2                       # the resident kernel took it
+    okids, omerged = orc.train_pnn(c.layers, act, c.init, K, c.lr, 0, X, y, threads=8)
+    assert np.abs(kids - okids).max() < TOL
+    assert np.abs(merged - omerged).max() < TOL
+    lab = net.predict(dev(Xt)).cpu().numpy()
+    np.testing.assert_array_equal(lab, orc.predict(c.layers, act, merged, Xt))
+
+
+def test_evaluate_matches_oracle(orc):
+    """f2 metrics (accuracy, confidence, cost; R29) of the merged net and of single
+    CNs, on the GPU's own trained parameters, vs the oracle's fp64 definitions."""
+    c = CONFIGS["C4"]
+    K = 8
+    X, y = make_split(K * 200, "train", 0)
+    Xt, yt = make_split(1003, "test", 0)
+    net, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y)
+    for sub, p in [(-1, merged), (0, kids[0]), (5, kids[5])]:
+        got = net.evaluate(dev(Xt), dev(yt), subnet=sub)
+        ref = orc.evaluate(c.layers, c.act, p, Xt, yt)
+        assert got[0] == ref[0]
+        np.testing.assert_allclose(got[1:], ref[1:], rtol=1e-12)
+    # sigmoid output (C2 shape): confidence / cost from φ_L
+    c2 = CONFIGS["C2"]
+    net2 = PNN(c2.layers, c2.act, c2.init, 1, c2.lr, seed=3)
+    got = net2.evaluate(dev(Xt), dev(yt))
+    ref = orc.evaluate(c2.layers, c2.act, net2.get_params(-1), Xt, yt)
+    assert got[0] == ref[0]
+    np.testing.assert_allclose(got[1:], ref[1:], rtol=1e-12)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_slots_do_not_change_results(kernel):
+    """f4: training in waves of `slots` CNs gives bit-identical CNs."""
+    c = CONFIGS["C4"]
+    K = 12
+    X, y = make_split(K * 40 + 5, "train", 0)
+    outs = []
+    for slots in (0, 1, 5):
+        net = PNN(c.layers, c.act, c.init, K, c.lr, seed=0, kernel=kernel)
+        net.set_slots(slots)
+        net.train_epoch(dev(X), dev(y))
+        torch.cuda.synchronize()
+        outs.append(np.stack([net.get_params(i) for i in range(K)]))
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
+
+
 def test_determinism_and_kernel_agreement(orc):
     c = CONFIGS["C4"]
     X, y = make_split(32 * 64, "train", 0)
@@ -141,12 +199,30 @@ def test_k1_is_snn_and_duplicated_shards(orc):
     np.testing.assert_array_equal(merged, kids[0])
 
 
-def test_minibatch_fp32(orc):
-    """Mini-batch GD, B=8 with a short last batch (R14)."""
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_minibatch_fp32(orc, kernel):
+    """Mini-batch GD, B=8 with a short last batch (R14), on the
+    reference kernel and the fp32 mini-batch step kernels (AUTO)."""
     c = CONFIGS["C4"]
     X, y = make_split(4 * 61, "train", 0)
-    _, kids, merged = _train(c.layers, c.act, c.init, 4, c.lr, X, y, batch=8)
+    net, kids, merged = _train(c.layers, c.act, c.init, 4, c.lr, X, y, batch=8, kernel=kernel)
+    assert net.kernel_info()[0] == (1 if kernel == "reference" else 4)
     okids, omerged = orc.train_pnn(c.layers, c.act, c.init, 4, c.lr, 0, X, y, batch=8)
+    assert np.abs(kids - okids).max() < TOL
+    assert np.abs(merged - omerged).max() < TOL
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_f1_paper_workload_reduced(orc, kernel):
+    """f1: the paper's own setting (784-256-10 ReLU/softmax, N(0,1) init, fp32
+    mini-batch B=50, η 0.1) on 3 CNs with ragged
+    slices and a short last batch, 2 epochs, vs the oracle."""
+    c = CONFIGS["F1"]
+    K, n = 3, 3 * (50 * 3 + 17) + 2
+    X, y = make_split(n, "train", 0)
+    _, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, epochs=2, batch=c.batch, kernel=kernel)
+    okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=2, batch=c.batch,
+                                   threads=K)
     assert np.abs(kids - okids).max() < TOL
     assert np.abs(merged - omerged).max() < TOL
 

@@ -19,6 +19,7 @@ ACT_PAIRS = [  # (hidden, output) — every activation/loss pair the configs use
     ("sigmoid", "softmax"),
     ("tanh", "tanh"),
     ("relu", "sigmoid"),
+    ("leaky_relu", "softmax"),   # f3 (slope 0.01, R28)
 ]
 
 
@@ -95,6 +96,26 @@ def test_relu_branch_points(orc):
     assert list(xs[0]) == [3.0, 0.0]
 
 
+def test_leaky_relu_branch_points(orc):
+    """Leaky ReLU (slope 0.01 by reading R28): φ(-1) = -0.01,
+    φ(0) = 0; at z = 0 the left slope 0.01 applies (as R9 takes ReLU'(0) = 0), so
+    unlike ReLU the unit at z = 0 passes 0.01 of its gradient (torch's
+    LeakyReLU derivative at 0 is also the left one)."""
+    params = np.array([0.0, 1.0, 0.0, -2.0, 1.0, 1.0, 0.0])
+    zs, xs = orc.forward([1, 2, 1], ["leaky_relu", "sigmoid"], params, [1.0])
+    assert list(zs[0]) == [0.0, -1.0]
+    assert xs[0][0] == 0.0 and xs[0][1] == -0.01
+    new = orc.train([1, 2, 1], ["leaky_relu", "sigmoid"], params, np.array([[1.0]]), np.array([0]),
+                    0.5, dtype=np.float64)
+    x2 = 1.0 / (1.0 + np.exp(-(0.0 * 1.0 + (-0.01) * 1.0)))
+    d2 = (x2 - 1.0) * x2 * (1.0 - x2)                       # Eq.9 with ½-SSE (R11)
+    np.testing.assert_allclose(new[0], 0.0 - 0.5 * (1.0 * d2 * 0.01) * 1.0, rtol=1e-12)
+    np.testing.assert_allclose(new[1], 1.0 - 0.5 * (1.0 * d2 * 0.01) * 1.0, rtol=1e-12)
+    t = torch.tensor([0.0, -1.0], dtype=torch.float64, requires_grad=True)
+    torch.nn.functional.leaky_relu(t, 0.01).sum().backward()
+    assert list(t.grad.numpy()) == [0.01, 0.01]
+
+
 def test_softmax_closed_forms(orc):
     """Eq.5: zero-weight/zero-bias net → uniform 1/10; CE of the
     uniform output = ln 10 (Eq.6); [1000,1000] → [.5,.5] without overflow (R4);
@@ -163,6 +184,8 @@ def _torch_net(layers, act, params):
             mods.append(torch.nn.Tanh())
         elif a == "relu":
             mods.append(torch.nn.ReLU())
+        elif a == "leaky_relu":
+            mods.append(torch.nn.LeakyReLU(0.01))
     return torch.nn.Sequential(*mods)
 
 

@@ -37,4 +37,9 @@ CONFIGS = {
     "C5": Config("C5", (784, 1024, 1024, 10), ("relu", "relu", "softmax"), "he", 8, 0.05,
                  480000, 10000, epochs=3, batch=64, precision="bf16",
                  note="init unstated; He-normal (ReLU)"),
+    # §8(f) f1: the paper's own workload: 784-256-10 ReLU +
+    # softmax/CE, N(0,1) init (the paper's NormFloat64, :209-213), fp32 mini-batch B=50,
+    # η 0.1 (Fig.3; Fig.2 uses 0.05), K=10 CNs, 20 epochs, 60k/10k rows
+    "F1": Config("F1", (784, 256, 10), ("relu", "softmax"), "normal", 10, 0.1, 60000, 10000,
+                 epochs=20, batch=50, note="paper's Fig.3 setting"),
 }
