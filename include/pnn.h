@@ -63,7 +63,7 @@ typedef enum {
  * layer.                                                                    */
 enum { PNN_SIGMOID = 0, PNN_TANH = 1, PNN_RELU = 2, PNN_SOFTMAX = 3,
        PNN_LEAKY_RELU = 4   /* φ(z) = z ≥ 0 ? z : 0.01·z (PAPER.md:281 names it, §5.2;
-                               slope unstated → 0.01, DESIGN.md §3 R28)          */ };
+                               slope unstated → 0.01, DESIGN.md §3 R30)          */ };
 
 /* Initialisation (reading R15).  Weights / biases:
  *   NORMAL         N(0,1) / N(0,1)          (the paper's NormFloat64)

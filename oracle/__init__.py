@@ -225,7 +225,7 @@ def evaluate(layers, act, params, X, y):
     * cost       = mean over rows of −log(max(x^L_y, 1e-12)) (Eq.6, PAPER.md:100-103:
       C = −Σ_i e_i log x_i with one-hot e; ε-clamp R29).
     x^L from the fp64 logits z^L: softmax exp(z − max z)/Σ (Eq.5 with R4), else φ_L(z)
-    (sigmoid 1/(1+e^−z), tanh, ReLU, leaky ReLU (R28) as in Eqs.3-4)."""
+    (sigmoid 1/(1+e^−z), tanh, ReLU, leaky ReLU (R30) as in Eqs.3-4)."""
     layers_, act_, L = _net(layers, act)
     labels, z = predict(layers, act, params, X, return_logits=True)
     a = int(act_[-1])

@@ -19,7 +19,7 @@ static REAL FN(act_scalar)(int act, REAL z) {
     case ORC_SIGMOID: return (REAL)1 / ((REAL)1 + EXP(-z));
     case ORC_TANH:    return TANH(z);
     case ORC_RELU:    return z >= (REAL)0 ? z : (REAL)0;      /* Eq.4: z>=0 → z */
-    /* leaky ReLU (§5.2; slope unstated → 0.01, reading R28)   */
+    /* leaky ReLU (§5.2; slope unstated → 0.01, reading R30)   */
     case ORC_LEAKY_RELU: return z >= (REAL)0 ? z : (REAL)0.01 * z;
     default:          return z;
     }
@@ -32,7 +32,7 @@ static REAL FN(act_deriv_from_x)(int act, REAL x) {
     case ORC_SIGMOID: return x * ((REAL)1 - x);
     case ORC_TANH:    return (REAL)1 - x * x;
     case ORC_RELU:    return x > (REAL)0 ? (REAL)1 : (REAL)0;
-    case ORC_LEAKY_RELU: return x > (REAL)0 ? (REAL)1 : (REAL)0.01;   /* R28: left slope at 0 (as R9) */
+    case ORC_LEAKY_RELU: return x > (REAL)0 ? (REAL)1 : (REAL)0.01;   /* R30: left slope at 0 (as R9) */
     default:          return (REAL)1;
     }
 }

@@ -11,7 +11,7 @@ __device__ __forceinline__ float act_fwd(int act, float z) {
     case PNN_SIGMOID: return 1.f / (1.f + expf(-z));
     case PNN_TANH: return tanhf(z);
     case PNN_RELU: return z >= 0.f ? z : 0.f;      // Eq.4
-    case PNN_LEAKY_RELU: return z >= 0.f ? z : 0.01f * z;   // R28
+    case PNN_LEAKY_RELU: return z >= 0.f ? z : 0.01f * z;   // R30
     default: return z;
     }
 }

@@ -114,7 +114,7 @@ def test_reduced_configs(orc, name, K, n, epochs, kernel):
 
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_leaky_relu_c4_shape(orc, kernel):
-    """f3: leaky ReLU hidden layer (slope 0.01, R28) on the C4 shape,
+    """f3: leaky ReLU hidden layer (slope 0.01, R30) on the C4 shape,
     reference and resident kernels vs the oracle."""
     c = CONFIGS["C4"]
     act = ["leaky_relu", "softmax"]

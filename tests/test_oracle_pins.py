@@ -19,7 +19,7 @@ ACT_PAIRS = [  # (hidden, output) — every activation/loss pair the configs use
     ("sigmoid", "softmax"),
     ("tanh", "tanh"),
     ("relu", "sigmoid"),
-    ("leaky_relu", "softmax"),   # f3 (slope 0.01, R28)
+    ("leaky_relu", "softmax"),   # f3 (slope 0.01, R30)
 ]
 
 
@@ -97,7 +97,7 @@ def test_relu_branch_points(orc):
 
 
 def test_leaky_relu_branch_points(orc):
-    """Leaky ReLU (slope 0.01 by reading R28): φ(-1) = -0.01,
+    """Leaky ReLU (slope 0.01 by reading R30): φ(-1) = -0.01,
     φ(0) = 0; at z = 0 the left slope 0.01 applies (as R9 takes ReLU'(0) = 0), so
     unlike ReLU the unit at z = 0 passes 0.01 of its gradient (torch's
     LeakyReLU derivative at 0 is also the left one)."""
