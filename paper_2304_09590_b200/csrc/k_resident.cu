@@ -66,7 +66,19 @@ constexpr int GR = 8;         // g ring slots (> LAG)
 static_assert(AR > LAG + 1 && GR > LAG, "ring sizes");
 constexpr int ZS = 4;         // partial-logit ring slots
 constexpr int CMAX = 4;       // cluster size
-constexpr int kTraceT = 64, kTraceP = 8;   // debug timeline: [cta][warp][t][point]
+#ifndef PNN_EXP_CHAIN_PAIRS
+#define PNN_EXP_CHAIN_PAIRS 4
+#endif
+#ifndef PNN_SWEEP_XWAIT
+#define PNN_SWEEP_XWAIT 1
+#endif
+// the chain warp of the pair that does not issue the x prefetch updates b2
+constexpr int kB2Half = PNN_SWEEP_XWAIT ? 1 : 0;
+// warp pairs that take turns running the chain: the highest-numbered ones (the warp
+// scheduler favours higher warp ids within an SM sub-partition)
+constexpr int kChainPairs = PNN_EXP_CHAIN_PAIRS;
+static_assert(kChainPairs == 1 || kChainPairs == 2 || kChainPairs == 4, "chain pairs");
+constexpr int kTraceT = 64, kTraceP = 16;   // debug timeline: [cta][warp][t][point]
 
 struct __align__(16) Smem {
     uint64_t xfull[S];                 // x(u) and its gram record landed
@@ -309,7 +321,11 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         if (warp < 4) {
         if (s < T) {
             // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
+#if PNN_SWEEP_XWAIT
+            mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));   // x(s) landed (usually long ago)
+#else
             if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
+#endif
             // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
             const float* xn = xring + sx * DP + 4 * lane;
             uint64_t acc[R];
@@ -317,8 +333,12 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             for (int r = 0; r < R; ++r) acc[r] = 0ull;
             uint64_t xa, xb;
             lds4(xn, xa, xb);
+#ifndef PNN_EXP_NO_SWEEP
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
+#else
+            for (int q = 0; q < 0; ++q) {
+#endif
                 uint64_t na = 0ull, nb = 0ull;
                 if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);   // one quad ahead
 #pragma unroll
@@ -371,8 +391,12 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
             uint64_t xa, xb;
             lds4(xo, xa, xb);
+#ifndef PNN_EXP_NO_SWEEP
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
+#else
+            for (int q = 0; q < 0; ++q) {
+#endif
                 uint64_t na = 0ull, nb = 0ull;
                 if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
 #pragma unroll
@@ -404,8 +428,12 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
             uint64_t xa, xb;
             lds4(xo, xa, xb);
+#ifndef PNN_EXP_NO_SWEEP
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
+#else
+            for (int q = 0; q < 0; ++q) {
+#endif
                 uint64_t na = 0ull, nb = 0ull;
                 if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
 #pragma unroll
@@ -425,7 +453,11 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         }
         if (s < T) {
             // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
+#if PNN_SWEEP_XWAIT
+            mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));   // x(s) landed (usually long ago)
+#else
             if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
+#endif
             // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
             const float* xn = xring + sx * DP + 4 * lane;
             uint64_t acc[R];
@@ -433,8 +465,12 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             for (int r = 0; r < R; ++r) acc[r] = 0ull;
             uint64_t xa, xb;
             lds4(xn, xa, xb);
+#ifndef PNN_EXP_NO_SWEEP
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
+#else
+            for (int q = 0; q < 0; ++q) {
+#endif
                 uint64_t na = 0ull, nb = 0ull;
                 if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);   // one quad ahead
 #pragma unroll
@@ -482,7 +518,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 #ifdef PNN_EXP_NO_CHAIN
         if (false) {
 #else
-        if (c >= 0 && c < T && (c & 3) == (warp >> 1)) {
+        if (c >= 0 && c < T && (c % kChainPairs) + (4 - kChainPairs) == (warp >> 1)) {
 #endif
             const int cs = (sx >= 1) ? sx - 1 : S - 1;          // ring slot of x(c)
             mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));   // every warp's row sums of c
@@ -499,6 +535,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
             z += sm.b1s[uc];
             const float h = lc ? act_fwd_t<A1>(z) : 0.f;
+            TR(7);
             // W2[o][uc] (pre-update: R6), kept for δ1 below
             float wv[12];
             {
@@ -528,6 +565,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 pv0 = (c1 ? pv[1] : pv[0]) + __shfl_xor_sync(0xffffffffu, c1 ? pv[0] : pv[1], 2);
                 pv0 += __shfl_xor_sync(0xffffffffu, pv0, 1);
             }
+            TR(8);
             // lane l now holds output (l >> 1) = 8·c4 + 4·c3 + 2·c2 + c1
             const int zs = c % ZS;
             {
@@ -546,14 +584,17 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                     else mbar_arrive(&sm.zfull[zs]);
                 }
             }
+            TR(9);
             // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
             //      which comes after their wait on gready(c) (first warp of the pair) ----
             // every warp has passed U(c-1) (aready(c) above): the slot of x(c-1-L) is free for x(c+PF)
+#if !PNN_SWEEP_XWAIT
             if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
             if (half == 0 && c + 2 + LAG < T) {
                 const int u = c + 2 + LAG;
                 mbar_wait(&sm.xfull[(cs + 2 + LAG) % S], (uint32_t)((u / S) & 1));
             }
+#endif
             TR(4);
             // ---- δ2(c) in every lane: z2 = Σ partials + b2(c) ----
             mbar_wait(&sm.zfull[zs], (uint32_t)((c / ZS) & 1));
@@ -594,6 +635,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
 #pragma unroll
                     for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
+                    TR(10);
                 } else {
 #pragma unroll
                     for (int o = 0; o < O; ++o) {
@@ -609,6 +651,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 for (int o = 0; o < O; ++o) s1 = fmaf(wv[o], dl[o], s1);
                 const float gu = lc ? lr * (s1 * act_deriv_t<A1>(h)) : 0.f;   // g(c) = η δ1
                 sm.gbuf[c % GR][uc] = gu;
+                TR(11);
                 sm.b1s[uc] -= gu;
 #pragma unroll
                 for (int o = 0; o < O; ++o) wv[o] = fmaf(-(lr * dl[o]), h, wv[o]);
@@ -617,7 +660,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
                 wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
             }
-            if (half == 0 && lane == 0) {              // b2(c+1) into the other buffer: the pair's
+            if (half == kB2Half && lane == 0) {        // b2(c+1) into the other buffer: the pair's
                 const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);   // partner may
                 float4* bq = reinterpret_cast<float4*>(&sm.b2s[(c + 1) & 1][0]);        // still read b2(c)
                 const float4 b0 = bo[0], b1v = bo[1], b2v = bo[2];
@@ -629,6 +672,11 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.gready[c % GR]);
+#if PNN_SWEEP_XWAIT
+            // off the critical path: every warp has passed U(c-1) (aready(c) above), so the
+            // slot of x(c-1-L) is free for x(c+PF); the sweeps wait for it themselves
+            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
+#endif
             TR(6);
         }
         if (++sx == S) sx = 0;

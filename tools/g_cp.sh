@@ -1,0 +1,7 @@
+#!/bin/bash
+cd /root/repo 2>/dev/null || cd "$(dirname "$0")/.."
+for v in "" _cp2 _cp1; do
+  echo "== variant '$v'"
+  PNN_LIB=$PWD/paper_2304_09590_b200/libpnn$v.so timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value']/1e6, d['roofline']['frac'], d['roofline']['train_ms_per_launch'], d['clocks']['sm_mhz'])"
+  PNN_LIB=$PWD/paper_2304_09590_b200/libpnn$v.so timeout 120 python tools/trace_resident.py --config C4 --K 148 --rows 256 2>&1 | grep -E "cta 0|chain period" | head -9
+done

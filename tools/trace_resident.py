@@ -26,7 +26,7 @@ a = ap.parse_args()
 c = CONFIGS[a.config]
 L = load()
 L.pnn_debug_set_trace.argtypes = [ctypes.c_void_p]
-NW, TT, PP = 8, 64, 8
+NW, TT, PP = 8, 64, 16
 buf = torch.zeros(2 * NW * TT * PP, dtype=torch.int64, device="cuda")
 X, y = make_split(a.K * a.rows, "train", 0)
 net = PNN(c.layers, c.act, c.init, a.K, c.lr)
@@ -49,6 +49,11 @@ for cta in range(2):
         if len(ch):
             cs = (f" | chain: wait {np.mean(ch[:, 3] - ch[:, 2]):.0f} publish {np.mean(ch[:, 4] - ch[:, 3]):.0f}"
                   f" xwait {0:.0f} exch {np.mean(ch[:, 5] - ch[:, 4]):.0f} finish {np.mean(ch[:, 6] - ch[:, 5]):.0f}")
+        if len(ch):
+            d = lambda a, b: np.mean(ch[:, b] - ch[:, a])
+            cs += (f"\n      publish = z1/h {d(3, 7):.0f} + W2/logits/reduce {d(7, 8):.0f} + store/st.async/arrive "
+                   f"{d(8, 9):.0f} + x issue/wait {d(9, 4):.0f}; finish = softmax {d(5, 10):.0f} + delta1/g "
+                   f"{d(10, 11):.0f} + updates/arrive {d(11, 6):.0f}")
         print(f"cta {cta} warp {w}: period {per:.0f} | F {f:.0f} U {u:.0f}{cs}")
 # chain period: time between consecutive chain completions (point 6 of the owning warp)
 done = []
