@@ -300,8 +300,18 @@ def main():
                                  "(0.6%) runs on CUDA cores",
                     "train_ms_per_launch": train_ms, "flop_per_launch": flop_launch}
         else:
+            traffic = None
+            try:      # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch,
+                      # from the committed ncu --set full capture of this workload
+                tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(cfg.name)
+                if tr and K_local == cfg.K and kernel_id == 2:
+                    traffic = tr["bytes_per_launch"]
+            except Exception:  # noqa: BLE001
+                traffic = None
             roof = {"bound": "alu", "achieved": achieved, "peak": peak_max,
-                    "unit": "TFLOP/s", "frac": achieved / peak_max, "traffic": None,
+                    "unit": "TFLOP/s", "frac": achieved / peak_max, "traffic": traffic,
+                    "traffic_note": "bytes/launch (ncu capture, profiles/ncu_traffic.json); algorithmic: "
+                                    "X 4·784·rows + 32-B Gram records·rows + 2·4·P_total·K",
                     "kernel": {1: "training epoch (reference kernel)",
                                2: "training epoch (Gram-term launch + persistent SGD launch)",
                                4: "training epoch (fp32 mini-batch: 4 launches per step, CUDA graph)"}

@@ -64,27 +64,41 @@ __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ childr
     const float* W1 = children + (long long)z * d.P + d.woff[1];
     const int tid = threadIdx.x, th = tid >> 4, tb = (tid & 15) * 4;   // thread: hidden h0+th, rows tb..tb+3
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k0 = 0; k0 < D; k0 += FK) {
-        // W1 tile [FH][FK]: 16 rows × 64 k = 256 float4 slots
-        {
-            const int r = tid >> 4, c = (tid & 15) * 4;
-            const int h = h0 + r, k = k0 + c;
-            // the CN slab (P floats) need not be 16-byte aligned: scalar loads
-            const float* src = W1 + (long long)h * D + k;
-            const bool ok = h < H && k < D;
+    // register-staged prefetch of the next k-tile while the current one is used
+    float wr[4];
+    float4 xr[4];
+    auto load_tile = [&](int k0) {
+        const int r = tid >> 4, c = (tid & 15) * 4;
+        const int h = h0 + r, k = k0 + c;
+        const float* src = W1 + (long long)h * D + k;   // the CN slab need not be 16-B aligned
+        const bool ok = h < H && k < D;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) ws[r][c + i] = ok ? src[i] : 0.f;
-        }
-        // x tile [64 rows][FK] -> xs[k][b]
+        for (int i = 0; i < 4; ++i) wr[i] = ok ? src[i] : 0.f;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int slot = tid + 256 * q;
-            const int b = slot >> 4, c = (slot & 15) * 4, k = k0 + c;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (b < bsz && k < D) v = *reinterpret_cast<const float4*>(X + (row0 + b) * D + k);
-            xs[c][b] = v.x; xs[c + 1][b] = v.y; xs[c + 2][b] = v.z; xs[c + 3][b] = v.w;
+            const int b = slot >> 4, cc = (slot & 15) * 4, kk = k0 + cc;
+            xr[q] = (b < bsz && kk < D) ? *reinterpret_cast<const float4*>(X + (row0 + b) * D + kk)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        __syncthreads();
+    };
+    auto store_tile = [&]() {
+        const int r = tid >> 4, c = (tid & 15) * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ws[r][c + i] = wr[i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int slot = tid + 256 * q;
+            const int b = slot >> 4, cc = (slot & 15) * 4;
+            xs[cc][b] = xr[q].x; xs[cc + 1][b] = xr[q].y; xs[cc + 2][b] = xr[q].z; xs[cc + 3][b] = xr[q].w;
+        }
+    };
+    load_tile(0);
+    store_tile();
+    __syncthreads();
+    for (int k0 = 0; k0 < D; k0 += FK) {
+        const bool more = k0 + FK < D;
+        if (more) load_tile(k0 + FK);
         const int kn = (D - k0) < FK ? (D - k0) : FK;
 #pragma unroll 8
         for (int k = 0; k < kn; ++k) {
@@ -96,6 +110,10 @@ __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ childr
             acc[3] = fmaf(w, xv.w, acc[3]);
         }
         __syncthreads();
+        if (more) {
+            store_tile();
+            __syncthreads();
+        }
     }
     const int h = h0 + th;
     if (h < H) {

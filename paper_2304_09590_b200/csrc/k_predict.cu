@@ -5,9 +5,9 @@
 // The forward pass (Eqs.2-3) runs in fp64 from the fp32 parameters (each
 // fp32×fp32 product is exact in fp64), so the argmax decision is taken in
 // fp64 on both the GPU and the oracle side (R26).  A CTA classifies
-// a tile of kTile samples: every weight is read once per tile (warp per
-// output neuron, lanes over inputs) and applied to the kTile activations held
-// in shared memory.
+// a tile of TILE samples: every weight is read once per tile (warp per
+// output neuron, lanes over inputs) and applied to the TILE activations held
+// in shared memory (inputs converted to fp64 once per tile).
 #include "pnn_internal.h"
 #include "pnn_device.cuh"
 
@@ -15,59 +15,65 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTile = 8;
 
-// EVAL: also the per-row evaluation terms of f2: the output
-// activation x^L (softmax max-subtracted, R4, or φ_L), its maximum (confidence,
-// reading R29) and the cross-entropy term −log(max(x^L_y, 1e-12)) (Eq.6, PAPER.md:100-103;
-// ε-clamp R29), plus whether the readout label equals y.
-template <bool EVAL>
+template <int TILE, bool EVAL>
 __global__ void __launch_bounds__(kThreads)
 predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restrict__ X,
                long long n, int32_t* __restrict__ labels, const int32_t* __restrict__ ytrue,
                double* __restrict__ rowstats) {
     extern __shared__ double smd[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int W = d.max_width;
-    double* bufA = smd;                       // [kTile][W]
-    double* bufB = smd + (size_t)kTile * W;   // [kTile][W]
-    for (long long t0 = (long long)blockIdx.x * kTile; t0 < n; t0 += (long long)gridDim.x * kTile) {
-        const int nt = (int)((n - t0) < kTile ? (n - t0) : kTile);
-        const int n0 = d.n[0];
-        for (int i = tid; i < kTile * n0; i += kThreads) {
+    const int n0 = d.n[0];
+    int Hm = 1;
+    for (int l = 1; l <= d.L; ++l) Hm = d.n[l] > Hm ? d.n[l] : Hm;
+    double* hb[2] = {smd, smd + (size_t)TILE * Hm};             // [TILE][Hm] fp64 activations
+    double* xin = smd + 2 * (size_t)TILE * Hm;                 // [TILE][n0] inputs, converted once
+    for (long long t0 = (long long)blockIdx.x * TILE; t0 < n; t0 += (long long)gridDim.x * TILE) {
+        const int nt = (int)((n - t0) < TILE ? (n - t0) : TILE);
+        for (int i = tid; i < TILE * n0; i += kThreads) {
             int s = i / n0, j = i % n0;
-            bufA[s * W + j] = (s < nt) ? (double)X[(t0 + s) * n0 + j] : 0.0;
+            xin[i] = (s < nt) ? (double)X[(t0 + s) * n0 + j] : 0.0;
         }
         __syncthreads();
-        double* in = bufA;
-        double* out = bufB;
+        const double* inD = nullptr;
+        int W = n0;
         for (int l = 1; l <= d.L; ++l) {
             const int nin = d.n[l - 1], nout = d.n[l];
             const float* Wl = params + d.woff[l];
             const float* bl = Wl + (long long)nout * nin;
+            double* out = hb[(l - 1) & 1];
             for (int k = warp; k < nout; k += kWarps) {
                 const float* w = Wl + (long long)k * nin;
-                double acc[kTile];
+                double acc[TILE];
 #pragma unroll
-                for (int s = 0; s < kTile; ++s) acc[s] = 0.0;
-                for (int j = lane; j < nin; j += 32) {
-                    const double wj = (double)w[j];
+                for (int s = 0; s < TILE; ++s) acc[s] = 0.0;
+                if (l == 1) {
+                    for (int j = lane; j < nin; j += 32) {
+                        const double wj = (double)w[j];
 #pragma unroll
-                    for (int s = 0; s < kTile; ++s) acc[s] = fma(wj, in[s * W + j], acc[s]);
+                        for (int s = 0; s < TILE; ++s) acc[s] = fma(wj, xin[s * W + j], acc[s]);
+                    }
+                } else {
+                    for (int j = lane; j < nin; j += 32) {
+                        const double wj = (double)w[j];
+#pragma unroll
+                        for (int s = 0; s < TILE; ++s) acc[s] = fma(wj, inD[s * Hm + j], acc[s]);
+                    }
                 }
 #pragma unroll
-                for (int s = 0; s < kTile; ++s) {
+                for (int s = 0; s < TILE; ++s) {
                     double z = warp_sum_d(acc[s]) + (double)bl[k];
                     // softmax is monotone: the readout only needs z^L (R19)
-                    if (lane == 0) out[s * W + k] = (l == d.L) ? z : act_fwd_d(d.act[l - 1], z);
+                    if (lane == 0) out[s * Hm + k] = (l == d.L) ? z : act_fwd_d(d.act[l - 1], z);
                 }
             }
             __syncthreads();
-            double* tmp = in; in = out; out = tmp;
+            inD = out;
+            W = Hm;
         }
-        // argmax over z^L (now in `in`), ties → lowest index
+        // argmax over z^L (now in inD), ties → lowest index
         if (tid < nt) {
-            const double* z = in + tid * W;
+            const double* z = inD + tid * Hm;
             int best = 0;
             for (int k = 1; k < d.n[d.L]; ++k) if (z[k] > z[best]) best = k;
             if (labels) labels[t0 + tid] = best;
@@ -112,22 +118,43 @@ __global__ void __launch_bounds__(1024) eval_reduce(const double* __restrict__ r
     if (threadIdx.x < 3) out[threadIdx.x] = sh[threadIdx.x][0] / (double)n;
 }
 
-template <bool EVAL>
-cudaError_t launch_pred(const NetDesc& d, const float* params, const float* x, long long n, int32_t* labels,
-                        const int32_t* ytrue, double* rowstats, cudaStream_t st) {
-    size_t smem = sizeof(double) * 2 * kTile * (size_t)d.max_width;
+template <int TILE, bool EVAL>
+size_t pred_smem(const NetDesc& d) {
+    int Hm = 1;
+    for (int l = 1; l <= d.L; ++l) Hm = d.n[l] > Hm ? d.n[l] : Hm;
+    return sizeof(double) * TILE * (2 * (size_t)Hm + (size_t)d.n[0]);
+}
+
+template <int TILE, bool EVAL>
+cudaError_t launch_pred_t(const NetDesc& d, const float* params, const float* x, long long n, int32_t* labels,
+                          const int32_t* ytrue, double* rowstats, cudaStream_t st) {
+    const size_t smem = pred_smem<TILE, EVAL>(d);
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(predict_kernel<EVAL>,
+        cudaError_t e = cudaFuncSetAttribute(predict_kernel<TILE, EVAL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    long long tiles = (n + kTile - 1) / kTile;
-    int grid = (int)(tiles < (long long)sms * 4 ? tiles : (long long)sms * 4);
-    predict_kernel<EVAL><<<grid, kThreads, smem, st>>>(d, params, x, n, labels, ytrue, rowstats);
+    const long long tiles = (n + TILE - 1) / TILE;
+    const int per_sm = smem > 110 * 1024 ? 1 : 2;
+    const int grid = (int)(tiles < (long long)sms * per_sm ? tiles : (long long)sms * per_sm);
+    predict_kernel<TILE, EVAL><<<grid, kThreads, smem, st>>>(d, params, x, n, labels, ytrue, rowstats);
     return cudaGetLastError();
+}
+
+// The tile (rows per CTA, each weight read once per tile) is the largest of 32/16/8 whose
+// fp64 input rows + two fp64 activation buffers fit in shared memory.
+template <bool EVAL>
+cudaError_t launch_pred(const NetDesc& d, const float* params, const float* x, long long n, int32_t* labels,
+                        const int32_t* ytrue, double* rowstats, cudaStream_t st) {
+    constexpr size_t kMax = 220 * 1024;
+    if (pred_smem<32, EVAL>(d) <= kMax) return launch_pred_t<32, EVAL>(d, params, x, n, labels, ytrue, rowstats, st);
+    if (pred_smem<16, EVAL>(d) <= kMax) return launch_pred_t<16, EVAL>(d, params, x, n, labels, ytrue, rowstats, st);
+    if (pred_smem<8, EVAL>(d) <= kMax) return launch_pred_t<8, EVAL>(d, params, x, n, labels, ytrue, rowstats, st);
+    if (pred_smem<2, EVAL>(d) <= kMax) return launch_pred_t<2, EVAL>(d, params, x, n, labels, ytrue, rowstats, st);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace
