@@ -291,14 +291,26 @@ def main():
         achieved = flop_launch / (train_ms / 1e3) / 1e12
         peak_max = sms * 128 * 2 * (pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         if cfg.precision == "bf16":
-            peak_tc = pk.get("bf16_tflops_sustained", 1392.3)
-            roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
-                    "frac": achieved / peak_tc, "traffic": None,
-                    "kernel": "training epoch (bf16 mini-batch: weight cast + 8 launches per step)",
-                    "peak_note": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS 8192^3 back to back); "
-                                 "flop = 2 x (3P - P1) per sample, of which the 10-wide output layer "
-                                 "(0.6%) runs on CUDA cores",
-                    "train_ms_per_launch": train_ms, "flop_per_launch": flop_launch}
+            # a10 is bound by the per-step fp32 master-weight update, not the tensor pipe:
+            # per mini-batch step and CN, the GEMM layers' weights (W1, W2) are read and written
+            # in fp32 (8 B), their bf16 copies written (W1b, W2b, W2bT: 2 B each) and read back by
+            # the next step's GEMMs (2 B each)  [DESIGN.md §5]
+            import math
+            W1 = cfg.layers[0] * cfg.layers[1]
+            W2 = cfg.layers[1] * cfg.layers[2]
+            bytes_step = K_local * (8 * (W1 + W2) + 2 * 2 * (W1 + 2 * W2))
+            steps_ep = math.ceil(math.ceil(nrows / K_local) / cfg.batch)
+            gbs = bytes_step * steps_ep / (train_ms / 1e3) / 1e9
+            hbm = pk.get("hbm_gbs", 6549.1)
+            tflops_tc = achieved
+            roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                    "traffic": None,
+                    "kernel": "training epoch (bf16 mini-batch: weight cast + 8 launches per step, CUDA graph)",
+                    "peak_note": "MEASURED_PEAKS.json hbm_gbs; algorithmic bytes per step = K_local x "
+                                 "(8(W1+W2) + 4(W1+2 W2)); tensor-side: "
+                                 f"{tflops_tc:.1f} TFLOP/s = {tflops_tc / pk.get('bf16_tflops_sustained', 1392.3):.3f} "
+                                 "of the sustained bf16 peak",
+                    "bytes_per_step": bytes_step, "train_ms_per_launch": train_ms, "flop_per_launch": flop_launch}
         else:
             traffic = None
             try:      # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch,

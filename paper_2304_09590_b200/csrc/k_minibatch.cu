@@ -98,7 +98,8 @@ extern "C" int pnn_debug_tc_gemm(const void* A, const void* B, float* C, int Z, 
 //   out_bwd  dW3 = δ3bᵀ·A2 -> W3, W3b; dA2 = δ3b·W3b(old); δ2 = dA2 ⊙ [A2 > 0] -> δ2b,
 //            δ2bT; b2 update
 //   B4 (tc)  dA1ᵀ = W2bT·δ2bᵀ (pre-update W2, R6); δ1 = dA1 ⊙ [A1T > 0] -> δ1T; b1 update
-//   B3 (tc)  dW2 = δ2bT·A1Tᵀ -> W2 -= η/B·dW2, W2b, W2bT
+//   B3 (tc)  dW2 = δ2bT·A1Tᵀ -> W2 -= η/B·dW2, W2b, W2bT (the other copy); runs on a side
+//            stream beside B4 -> B5 (it only has to finish before the next step's F1)
 //   B5 (tc)  dW1 = δ1T·XsTᵀ  -> W1 -= η/B·dW1, W1b
 // =====================================================================================
 
@@ -106,8 +107,11 @@ struct MbState {
     int K_local, D, H1, H2, O, B;
     long long P, woff1, woff2, woff3;
     __nv_bfloat16 *W1b, *W2b, *W2bT, *W3b, *Xs, *XsT, *A1, *A1T, *A2, *d2b, *d2bT, *d1T, *d3b;
+    __nv_bfloat16* W2bT2;     // second W2ᵀ copy: step j's B4 reads [j & 1] while B3 writes the other
     float* d3;
-    CUtensorMap tW1b, tXs, tW2b, tA1, tW2bT, td2b, td2bT, tA1T, td1T, tXsT;
+    CUtensorMap tW1b, tXs, tW2b, tA1, tW2bT, td2b, td2bT, tA1T, td1T, tXsT, tW2bT2;
+    cudaStream_t side = nullptr;          // B3 runs beside B4 -> B5 (forked inside the graph)
+    cudaEvent_t ev_ob = nullptr, ev_b3 = nullptr;
     // the epoch's launch sequence as a CUDA graph, re-used while its arguments are unchanged
     // (a small cache: the host-input path trains the CNs in a few groups)
     cudaStream_t cap = nullptr;
@@ -149,13 +153,16 @@ const char* mb_plan(const NetDesc& d, int batch) {
 
 void mb_destroy(MbState* s) {
     if (!s) return;
-    __nv_bfloat16* bufs[] = {s->W1b, s->W2b, s->W2bT, s->W3b, s->Xs, s->XsT, s->A1, s->A1T, s->A2, s->d2b,
+    __nv_bfloat16* bufs[] = {s->W2bT2, s->W1b, s->W2b, s->W2bT, s->W3b, s->Xs, s->XsT, s->A1, s->A1T, s->A2, s->d2b,
                              s->d2bT, s->d1T, s->d3b};
     for (auto* b : bufs) cudaFree(b);
     cudaFree(s->d3);
     for (auto& e : s->g)
         if (e.exec) cudaGraphExecDestroy(e.exec);
     if (s->cap) cudaStreamDestroy(s->cap);
+    if (s->side) cudaStreamDestroy(s->side);
+    if (s->ev_ob) cudaEventDestroy(s->ev_ob);
+    if (s->ev_b3) cudaEventDestroy(s->ev_b3);
     delete s;
 }
 
@@ -166,7 +173,7 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     s->P = d.P; s->woff1 = d.woff[1]; s->woff2 = d.woff[2]; s->woff3 = d.woff[3];
     const long long Z = K_local, D = s->D, H1 = s->H1, H2 = s->H2, B = s->B;
     struct { __nv_bfloat16** p; long long n; } al[] = {
-        {&s->W1b, Z * H1 * D}, {&s->W2b, Z * H2 * H1}, {&s->W2bT, Z * H1 * H2}, {&s->W3b, Z * 16 * H2},
+        {&s->W1b, Z * H1 * D}, {&s->W2b, Z * H2 * H1}, {&s->W2bT, Z * H1 * H2}, {&s->W2bT2, Z * H1 * H2}, {&s->W3b, Z * 16 * H2},
         {&s->Xs, Z * B * D}, {&s->XsT, Z * D * B}, {&s->A1, Z * B * H1}, {&s->A1T, Z * H1 * B},
         {&s->A2, Z * B * H2}, {&s->d2b, Z * B * H2}, {&s->d2bT, Z * H2 * B}, {&s->d1T, Z * H1 * B},
         {&s->d3b, Z * B * 16}};
@@ -176,6 +183,9 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     if (*err == cudaSuccess) *err = cudaMalloc(&s->d3, sizeof(float) * (size_t)(Z * B * 16));
     if (*err == cudaSuccess) *err = cudaMemset(s->W3b, 0, sizeof(__nv_bfloat16) * (size_t)(Z * 16 * H2));
     if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
+    if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+    if (*err == cudaSuccess) *err = cudaEventCreateWithFlags(&s->ev_ob, cudaEventDisableTiming);
+    if (*err == cudaSuccess) *err = cudaEventCreateWithFlags(&s->ev_b3, cudaEventDisableTiming);
     if (*err == cudaSuccess) *err = prepare_gemm_attrs();
     bool ok = *err == cudaSuccess;
     const int iZ = (int)Z;
@@ -184,6 +194,7 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     ok = ok && make_tmap_kmajor(&s->tW2b, s->W2b, (int)H1, (int)H2, iZ, tc::BM);
     ok = ok && make_tmap_kmajor(&s->tA1, s->A1, (int)H1, (int)B, iZ, (int)B);
     ok = ok && make_tmap_kmajor(&s->tW2bT, s->W2bT, (int)H2, (int)H1, iZ, tc::BM);
+    ok = ok && make_tmap_kmajor(&s->tW2bT2, s->W2bT2, (int)H2, (int)H1, iZ, tc::BM);
     ok = ok && make_tmap_kmajor(&s->td2b, s->d2b, (int)H2, (int)B, iZ, (int)B);
     ok = ok && make_tmap_kmajor(&s->td2bT, s->d2bT, (int)B, (int)H2, iZ, tc::BM);
     ok = ok && make_tmap_kmajor(&s->tA1T, s->A1T, (int)B, (int)H1, iZ, 256);
@@ -421,6 +432,8 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
     base.batch = B;
     for (long long j = 0; j < steps; ++j) {
         base.step = (int)j;
+        // B3 of step j-1 (side stream) still reads A1T / δ2bT and writes W2b: join before F1(j)
+        if (j > 0 && (e = cudaStreamWaitEvent(st, s->ev_b3, 0))) return e;
         mb_cast_x<<<dim3((unsigned)((s->D + 63) / 64), (unsigned)s_count), 256, 0, st>>>(x, *s, n_local, K_local,
                                                                                       s_first, (int)j);
         // F1: A1 = relu(W1b·Xsᵀ + b1)
@@ -440,18 +453,24 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
                                                                                  s_first, (int)j);
         mb_out_bwd<<<dim3((unsigned)(s->H2 / 64), (unsigned)s_count), 256, 0, st>>>(
             children, *s, n_local, K_local, s_first, (int)j, lr);
+        if ((e = cudaEventRecord(s->ev_ob, st))) return e;
+        const bool odd = (j & 1) != 0;
         // B4: δ1 = (W2bᵀ·δ2b) ⊙ [A1 > 0]; b1 update (pre-update W2: before B3)
         tc::Epi b4 = base;
         b4.M = s->H1; b4.N = B; b4.nvalid = B;
         b4.mask = s->A1T; b4.out_mb = s->d1T; b4.zs_act = (long long)s->H1 * B;
         b4.bias_upd = children + s->woff1 + (long long)s->H1 * s->D; b4.zs_bias = s->P;
-        if ((e = launch_gemm<64, tc::EPI_BWD>(s->tW2bT, s->td2b, s_count, s->H1, B, s->H2, b4, st))) return e;
+        if ((e = launch_gemm<64, tc::EPI_BWD>(odd ? s->tW2bT2 : s->tW2bT, s->td2b, s_count, s->H1, B, s->H2, b4,
+                                                st)))
+            return e;
         // B3: W2 -= η/B · δ2bᵀ·A1
         tc::Epi b3 = base;
         b3.M = s->H2; b3.N = s->H1; b3.nvalid = s->H1;
         b3.master = children + s->woff2; b3.zs_master = s->P;
-        b3.wb = s->W2b; b3.wbt = s->W2bT; b3.zs_w = (long long)s->H2 * s->H1;
-        if ((e = launch_gemm<256, tc::EPI_UPD>(s->td2bT, s->tA1T, s_count, s->H2, s->H1, B, b3, st))) return e;
+        b3.wb = s->W2b; b3.wbt = odd ? s->W2bT : s->W2bT2; b3.zs_w = (long long)s->H2 * s->H1;
+        if ((e = cudaStreamWaitEvent(s->side, s->ev_ob, 0))) return e;
+        if ((e = launch_gemm<256, tc::EPI_UPD>(s->td2bT, s->tA1T, s_count, s->H2, s->H1, B, b3, s->side))) return e;
+        if ((e = cudaEventRecord(s->ev_b3, s->side))) return e;
         // B5: W1 -= η/B · δ1ᵀ·Xs
         tc::Epi b5 = base;
         b5.M = s->H1; b5.N = s->D; b5.nvalid = s->D;
@@ -459,6 +478,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         b5.wb = s->W1b; b5.wbt = nullptr; b5.zs_w = (long long)s->H1 * s->D;
         if ((e = launch_gemm<256, tc::EPI_UPD>(s->td1T, s->tXsT, s_count, s->H1, s->D, B, b5, st))) return e;
     }
+    if (steps > 0 && (e = cudaStreamWaitEvent(st, s->ev_b3, 0))) return e;   // join the side stream
     return cudaGetLastError();
 }
 
