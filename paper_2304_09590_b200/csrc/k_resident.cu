@@ -69,6 +69,12 @@ constexpr int CMAX = 4;       // cluster size
 #ifndef PNN_EXP_CHAIN_PAIRS
 #define PNN_EXP_CHAIN_PAIRS 4
 #endif
+#ifndef PNN_CHAIN_V9
+#define PNN_CHAIN_V9 0
+#endif
+// v9 chain: the pair publishes h to shared memory and one warp forms the CTA's partial
+// logits lane-per-output (one row per CTA instead of a transpose-reduce row per warp)
+constexpr bool kV9 = PNN_CHAIN_V9 != 0;
 #ifndef PNN_SWEEP_XWAIT
 #define PNN_SWEEP_XWAIT 1
 #endif
@@ -88,7 +94,8 @@ struct __align__(16) Smem {
     float asum[AR][UMAX][4];           // [s % AR][row][part] partial row sums of acc(s)
     float gbuf[GR][UMAX];              // [c % GR][row] g(c)
     float zbuf[ZS][2 * CMAX][16];      // [c % ZS][2·cta + half][o] partial logits
-    float w2s[UMAX][16];               // W2[o][k0 + u] (o < 10), the CTA's units
+    float w2s[UMAX][16];               // W2[o][k0 + u] (o < 10), the CTA's units (v8 layout)
+    float w2t[16][UMAX + 4];           // the same, output-major (v9 layout; padded rows)
     float b1s[UMAX];                   // b1 of the CTA's units
     float b2s[2][16];                  // b2 before sample c at [c & 1] (identical in every CTA)
     float hs[2][UMAX];                 // h(c) of the CTA's units, [c & 1]
@@ -236,7 +243,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
         for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NW);
         for (int i = 0; i < GR; ++i) mbar_init(&sm.gready[i], 2);
-        for (int i = 0; i < ZS; ++i) mbar_init(&sm.zfull[i], 2);
+        for (int i = 0; i < ZS; ++i) mbar_init(&sm.zfull[i], kV9 ? 1 : 2);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < (S + 1) * DP; i += blockDim.x) xring[i] = 0.f;   // + zero row
@@ -244,7 +251,9 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 
     for (int i = threadIdx.x; i < UMAX * 16; i += blockDim.x) {
         const int u = i >> 4, o = i & 15;
-        sm.w2s[u][o] = (u < Uown && o < O) ? W2[(long long)o * H + k0 + u] : 0.f;
+        const float wv0 = (u < Uown && o < O) ? W2[(long long)o * H + k0 + u] : 0.f;
+        sm.w2s[u][o] = wv0;
+        sm.w2t[o][u] = wv0;
     }
     for (int i = threadIdx.x; i < UMAX; i += blockDim.x) sm.b1s[i] = (i < Uown) ? b1g[k0 + i] : 0.f;
     for (int i = threadIdx.x; i < 32; i += blockDim.x) (&sm.b2s[0][0])[i] = (i < O) ? b2g[i] : 0.f;
@@ -302,7 +311,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     const int half = warp & 1;
     const int uc = 32 * half + lane;               // this lane's unit in the chain
     const bool lc = uc < Uown;
-    const int zrow = 2 * crank + half;             // this warp's row of zbuf in every CTA
+    const int zrow = kV9 ? crank : 2 * crank + half;   // this warp's / CTA's row of zbuf in every CTA
     uint32_t rz[C > 1 ? C - 1 : 1];                // DSMEM address of zbuf[0][zrow][0] in each peer
     if constexpr (C > 1) {
 #pragma unroll
@@ -538,6 +547,40 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             TR(7);
             // W2[o][uc] (pre-update: R6), kept for δ1 below
             float wv[12];
+            const int zs = c % ZS;
+            if constexpr (kV9) {
+#pragma unroll
+                for (int o = 0; o < 12; ++o) wv[o] = (o < O) ? sm.w2t[o][uc] : 0.f;
+                sm.hs[c & 1][uc] = h;
+                named_bar_sync(1 + (warp >> 1), 64);      // the pair's h(c) is in shared memory (ids 1..4)
+                TR(8);
+                if (half == 0) {
+                    // ---- the CTA's partial logits, lane o: Σ_u W2[o][u] h_u over the 64 units ----
+                    const int o = lane < O ? lane : 0;
+                    const float4* wr = reinterpret_cast<const float4*>(&sm.w2t[o][0]);
+                    const float4* hr = reinterpret_cast<const float4*>(&sm.hs[c & 1][0]);
+                    float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+                    for (int q = 0; q < UMAX / 4; ++q) {
+                        const float4 w4 = wr[q], h4 = hr[q];
+                        a[q & 3] = fmaf(w4.w, h4.w, fmaf(w4.z, h4.z, fmaf(w4.y, h4.y, fmaf(w4.x, h4.x, a[q & 3]))));
+                    }
+                    const float zl = (a[0] + a[1]) + (a[2] + a[3]);
+                    const bool pub = lane < O;
+                    if (pub) sm.zbuf[zs][zrow][lane] = zl;
+                    if constexpr (C > 1) {
+#pragma unroll
+                        for (int p = 0; p < C - 1; ++p)
+                            st_async_f32_if(pub, rz[p] + zs * kZStride + lane * 4, zl,
+                                            rz[p] + kZfullOff - (uint32_t)(zrow * 64) + zs * 8);
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (C > 1) mbar_arrive_expect_tx(&sm.zfull[zs], (uint32_t)((C - 1) * O * 4));
+                        else mbar_arrive(&sm.zfull[zs]);
+                    }
+                }
+            } else {
             {
                 const float4* wq = reinterpret_cast<const float4*>(&sm.w2s[uc][0]);
 #pragma unroll
@@ -567,7 +610,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             }
             TR(8);
             // lane l now holds output (l >> 1) = 8·c4 + 4·c3 + 2·c2 + c1
-            const int zs = c % ZS;
             {
                 const int oi = lane >> 1;
                 const bool pub = (lane & 1) == 0 && oi < O;
@@ -583,6 +625,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                     if constexpr (C > 1) mbar_arrive_expect_tx(&sm.zfull[zs], (uint32_t)((C - 1) * O * 4));
                     else mbar_arrive(&sm.zfull[zs]);
                 }
+            }
             }
             TR(9);
             // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
@@ -614,7 +657,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 #pragma unroll
                 for (int o = 0; o < 12; ++o) zp[o] = 0.f;
 #pragma unroll
-                for (int i = 0; i < 2 * C; ++i) {
+                for (int i = 0; i < (kV9 ? C : 2 * C); ++i) {
                     const float4* zq = reinterpret_cast<const float4*>(&sm.zbuf[zs][i][0]);
 #pragma unroll
                     for (int q = 0; q < 3; ++q) {
@@ -625,12 +668,13 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 #pragma unroll
                 for (int o = 0; o < 12; ++o) z2[o] += zp[o];                // z2 = W2 h + b2 (Eq.2)
                 if constexpr (A2 == PNN_SOFTMAX) {
-                    float m = z2[0];
+                    // max and sum as trees (O = 10: depth 4 instead of 9)
+                    const float m = fmaxf(fmaxf(fmaxf(z2[0], z2[1]), fmaxf(z2[2], z2[3])),
+                                          fmaxf(fmaxf(fmaxf(z2[4], z2[5]), fmaxf(z2[6], z2[7])), fmaxf(z2[8], z2[9])));
 #pragma unroll
-                    for (int o = 1; o < O; ++o) m = fmaxf(m, z2[o]);
-                    float sum = 0.f;
-#pragma unroll
-                    for (int o = 0; o < O; ++o) { dl[o] = __expf(z2[o] - m); sum += dl[o]; }
+                    for (int o = 0; o < O; ++o) dl[o] = __expf(z2[o] - m);
+                    const float sum = ((dl[0] + dl[1]) + (dl[2] + dl[3])) +
+                                      (((dl[4] + dl[5]) + (dl[6] + dl[7])) + (dl[8] + dl[9]));
                     float inv;
                     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
 #pragma unroll
@@ -655,10 +699,15 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 sm.b1s[uc] -= gu;
 #pragma unroll
                 for (int o = 0; o < O; ++o) wv[o] = fmaf(-(lr * dl[o]), h, wv[o]);
-                float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
-                wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
-                wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
-                wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
+                if constexpr (kV9) {
+#pragma unroll
+                    for (int o = 0; o < O; ++o) sm.w2t[o][uc] = wv[o];
+                } else {
+                    float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
+                    wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+                    wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
+                    wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
+                }
             }
             if (half == kB2Half && lane == 0) {        // b2(c+1) into the other buffer: the pair's
                 const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);   // partner may
@@ -705,7 +754,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     float* W2o = opaque(W2);
     for (int i = threadIdx.x; i < Uown * O; i += blockDim.x) {
         const int u = i / O, o = i % O;
-        W2o[(long long)o * H + k0 + u] = sm.w2s[u][o];
+        W2o[(long long)o * H + k0 + u] = kV9 ? sm.w2t[o][u] : sm.w2s[u][o];
     }
     for (int i = threadIdx.x; i < Uown; i += blockDim.x) opaque(b1g)[k0 + i] = sm.b1s[i];
     if (crank == 0 && threadIdx.x < O) opaque(b2g)[threadIdx.x] = sm.b2s[T & 1][threadIdx.x];

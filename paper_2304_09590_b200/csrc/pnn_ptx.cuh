@@ -121,6 +121,10 @@ __device__ __forceinline__ uint32_t cluster_nctarank() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// named barrier `id` (1..15) over `nthreads` threads (a multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ long long clock64() {
     long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
