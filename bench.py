@@ -171,7 +171,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "reference", "resident"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "reference", "resident", "cluster"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -326,6 +326,7 @@ def main():
                                     "X 4·784·rows + 32-B Gram records·rows + 2·4·P_total·K",
                     "kernel": {1: "training epoch (reference kernel)",
                                2: "training epoch (Gram-term launch + persistent SGD launch)",
+                               5: "training epoch (cluster kernel, weights in cluster shared memory)",
                                4: "training epoch (fp32 mini-batch: 4 launches per step, CUDA graph)"}
                               .get(kernel_id, "training epoch"),
                     "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
@@ -353,7 +354,7 @@ def main():
                                    f"{cfg.n_train} rows, {cfg.epochs} epoch(s), batch {cfg.batch}, "
                                    f"lr {cfg.lr}",
                        "K_local": K_local, "rows_per_rank": nrows, "test_rows": cfg.n_test,
-                       "kernel": ["auto", "reference", "resident", "tc_bf16", "mb_f32"][kernel_id],
+                       "kernel": ["auto", "reference", "resident", "tc_bf16", "mb_f32", "cluster"][kernel_id],
                        "l2": f"inputs {X.nbytes / 2**20:.0f} MiB per rank > 126 MB L2 (no flush)"},
             "roofline": roof,
             "breakdown_ms": {"train": train_ms * cfg.epochs, "merge_predict": ms - train_ms * cfg.epochs},

@@ -85,9 +85,13 @@ enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          
        PNN_KERNEL_TC_BF16 = 3,   /* bf16 mini-batch on tcgen05 GEMMs; chosen by
                                     pnn_set_minibatch(.., PNN_BF16), reported
                                     by pnn_kernel_info, not settable         */
-       PNN_KERNEL_MB_F32 = 4     /* fp32 mini-batch step kernels (D-H-O nets,
+       PNN_KERNEL_MB_F32 = 4,    /* fp32 mini-batch step kernels (D-H-O nets,
                                     batch 2..64; AUTO picks it, REFERENCE
-                                    opts out), reported, not settable        */ };
+                                    opts out), reported, not settable        */
+       PNN_KERNEL_CLUSTER = 5    /* per-sample SGD, any depth, weights resident
+                                    in the shared memory of a cluster of <= 8
+                                    CTAs (AUTO's choice when the resident
+                                    kernel does not cover the shape, e.g. C3) */ };
 
 /* Build a PNN of n_subnets CNs with layer sizes layers[0..n_layers-1]
  * (layers[0] = inputs, e.g. {784,128,10}; n_layers >= 2, each size >= 1,
@@ -127,8 +131,9 @@ pnn_status pnn_set_comm(pnn_net net, const void* nccl_unique_id, int32_t nranks,
  * outside the list above — the message names the violated condition).     */
 pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision);
 
-/* Force a training kernel (PNN_KERNEL_*).  PNN_KERNEL_RESIDENT returns
- * PNN_ERR_INVALID when the shape does not fit it.        */
+/* Force a training kernel (PNN_KERNEL_AUTO, _REFERENCE, _RESIDENT or _CLUSTER).
+ * PNN_KERNEL_RESIDENT / _CLUSTER return PNN_ERR_INVALID when the shape does
+ * not fit them; _TC_BF16 and _MB_F32 are not settable.    */
 pnn_status pnn_set_kernel(pnn_net net, int32_t kernel);
 
 /* Limit how many local CNs train concurrently (the GPU

@@ -164,9 +164,11 @@ int choose_kernel(pnn_net net, ResidentPlan* plan) {
     if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1 && !mb32_plan(net->d, net->batch))
         return PNN_KERNEL_MB_F32;
     if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
+    if (net->kernel == PNN_KERNEL_CLUSTER) return plan_cluster(net->d, net->batch).ok ? PNN_KERNEL_CLUSTER : -1;
     *plan = plan_resident(net->d, net->batch);
     if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
-    return plan->ok ? PNN_KERNEL_RESIDENT : PNN_KERNEL_REFERENCE;
+    if (plan->ok) return PNN_KERNEL_RESIDENT;
+    return plan_cluster(net->d, net->batch).ok ? PNN_KERNEL_CLUSTER : PNN_KERNEL_REFERENCE;
 }
 
 pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long long n,
@@ -189,7 +191,7 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
                              int s_first, int s_count, cudaStream_t st) {
     ResidentPlan plan{};
     int k = choose_kernel(net, &plan);
-    if (k < 0) return fail(net, PNN_ERR_INVALID, "resident kernel not valid here: %s", plan.why);
+    if (k < 0) return fail(net, PNN_ERR_INVALID, "forced kernel not valid here: %s", plan.why);
     cudaError_t e;
     if (k == PNN_KERNEL_TC_BF16) {
         if (!net->mb) {
@@ -209,6 +211,9 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         }
         e = launch_minibatch_f32(net->mb32, net->d, net->d_children, x, y, n, net->K_local, s_first, s_count,
                                  net->lr, st);
+    } else if (k == PNN_KERNEL_CLUSTER) {
+        const ClusterPlan cp = plan_cluster(net->d, net->batch);
+        e = launch_sgd_cluster(cp, net->d, net->d_children, x, y, n, net->K_local, s_first, s_count, net->lr, st);
     } else if (k == PNN_KERNEL_RESIDENT) {
         if (net->gram_rows < n) {
             cudaFree(net->d_gram);
@@ -360,8 +365,13 @@ pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision) {
 pnn_status pnn_set_kernel(pnn_net net, int32_t kernel) {
     pnn_status st = check_live(net);
     if (st) return st;
-    if (kernel < PNN_KERNEL_AUTO || kernel > PNN_KERNEL_RESIDENT)
-        return fail(net, PNN_ERR_INVALID, "kernel = %d unknown", kernel);
+    if (kernel < PNN_KERNEL_AUTO || kernel > PNN_KERNEL_CLUSTER || kernel == PNN_KERNEL_TC_BF16 ||
+        kernel == PNN_KERNEL_MB_F32)
+        return fail(net, PNN_ERR_INVALID, "kernel = %d unknown or not settable", kernel);
+    if (kernel == PNN_KERNEL_CLUSTER) {
+        ClusterPlan p = plan_cluster(net->d, net->batch);
+        if (!p.ok) return fail(net, PNN_ERR_INVALID, "cluster kernel not valid: %s", p.why);
+    }
     if (kernel == PNN_KERNEL_RESIDENT) {
         ResidentPlan p = plan_resident(net->d, net->batch);
         if (!p.ok) return fail(net, PNN_ERR_INVALID, "resident kernel not valid: %s", p.why);

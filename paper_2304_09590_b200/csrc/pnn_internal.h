@@ -58,6 +58,19 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 int K_local, int s_first, int s_count, float lr,
                                 cudaStream_t st);
 
+// Cluster kernel (k_cluster.cu): any depth, weights resident in the shared memory of a
+// cluster of C <= 8 CTAs, per-sample SGD.
+struct ClusterPlan {
+    bool ok;
+    int cluster;
+    size_t smem;
+    char why[160];
+};
+ClusterPlan plan_cluster(const NetDesc& d, int batch);
+cudaError_t launch_sgd_cluster(const ClusterPlan& p, const NetDesc& d, float* children, const float* x,
+                               const int32_t* labels, long long n_local, int K_local, int s_first,
+                               int s_count, float lr, cudaStream_t st);
+
 // bf16 mini-batch variant on tcgen05 GEMMs (k_minibatch.cu): nullptr when the shape /
 // batch is supported, else the reason.
 struct MbState;

@@ -22,13 +22,14 @@ STATUS_NAMES = ["PNN_OK", "PNN_ERR_INVALID", "PNN_ERR_SHAPE", "PNN_ERR_DATA", "P
 PNN_SIGMOID, PNN_TANH, PNN_RELU, PNN_SOFTMAX, PNN_LEAKY_RELU = 0, 1, 2, 3, 4
 PNN_INIT_NORMAL, PNN_INIT_UNIFORM, PNN_INIT_XAVIER_NORMAL, PNN_INIT_HE_NORMAL = 0, 1, 2, 3
 PNN_FP32, PNN_BF16 = 0, 1
-PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16, PNN_KERNEL_MB_F32 = \
-    0, 1, 2, 3, 4
+PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16, PNN_KERNEL_MB_F32, \
+    PNN_KERNEL_CLUSTER = 0, 1, 2, 3, 4, 5
 ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX,
        "leaky_relu": PNN_LEAKY_RELU}
 INIT = {"normal": PNN_INIT_NORMAL, "uniform": PNN_INIT_UNIFORM, "xavier": PNN_INIT_XAVIER_NORMAL,
         "he": PNN_INIT_HE_NORMAL}
-KERNEL = {"auto": PNN_KERNEL_AUTO, "reference": PNN_KERNEL_REFERENCE, "resident": PNN_KERNEL_RESIDENT}
+KERNEL = {"auto": PNN_KERNEL_AUTO, "reference": PNN_KERNEL_REFERENCE, "resident": PNN_KERNEL_RESIDENT,
+          "cluster": PNN_KERNEL_CLUSTER}
 
 EXPORTS = ["pnn_create", "pnn_set_comm", "pnn_set_minibatch", "pnn_set_kernel", "pnn_train_epoch",
            "pnn_train_epoch_host", "pnn_merge", "pnn_predict", "pnn_get_params", "pnn_set_params",

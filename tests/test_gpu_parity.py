@@ -170,6 +170,20 @@ def test_slots_do_not_change_results(kernel):
     np.testing.assert_array_equal(outs[0], outs[2])
 
 
+@pytest.mark.parametrize("name,K,n,epochs", REDUCED + [("C1", 2, 2 * 300 + 1, 1)])
+def test_cluster_kernel(orc, name, K, n, epochs):
+    """The cluster kernel (weights in the shared memory of a cluster of CTAs, any
+    depth; AUTO's choice for C3) forced on every config shape, vs the oracle."""
+    c = CONFIGS[name]
+    X, y = make_split(n, "train", 0)
+    net, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, epochs, "cluster")
+    assert net.kernel_info()[0] == 5
+    okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=epochs, threads=8)
+    err = np.abs(kids - okids).max(axis=1)
+    assert err.max() < TOL, f"per-CN max-abs {err}"
+    assert np.abs(merged - omerged).max() < TOL
+
+
 def test_determinism_and_kernel_agreement(orc):
     c = CONFIGS["C4"]
     X, y = make_split(32 * 64, "train", 0)
