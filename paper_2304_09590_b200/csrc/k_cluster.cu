@@ -189,6 +189,23 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         for (long long t = 0; t < kAhead && t < T; ++t) issue(t);
     cluster_sync_all();                            // peers' barriers are live before any remote store
 
+    // per-layer tables in shared memory: indexing kernel parameters by a runtime layer
+    // number compiles to slow indexed constant loads on the per-sample path
+    __shared__ struct {
+        int n[PNN_MAX_LAYERS + 1], act[PNN_MAX_LAYERS + 1], rows[PNN_MAX_LAYERS + 1];
+        int w_off[PNN_MAX_LAYERS + 1], b_off[PNN_MAX_LAYERS + 1], x_off[PNN_MAX_LAYERS + 1],
+            d_off[PNN_MAX_LAYERS + 1];
+    } sp;
+    if (tid <= PNN_MAX_LAYERS) {
+        sp.n[tid] = d.n[tid];
+        sp.act[tid] = tid < PNN_MAX_LAYERS ? d.act[tid] : 0;
+        sp.rows[tid] = pl.rows[tid];
+        sp.w_off[tid] = pl.w_off[tid];
+        sp.b_off[tid] = pl.b_off[tid];
+        sp.x_off[tid] = pl.x_off[tid];
+        sp.d_off[tid] = pl.d_off[tid];
+    }
+    __syncthreads();
     const uint32_t sbase = smem_u32(smf);
     int label_next = (T > 0) ? Y[row0] : 0;        // labels are loaded one sample ahead
 #ifdef PNN_CLUSTER_PROFILE
@@ -209,10 +226,10 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         const float* x0 = smf + pl.ring_off + slot * pl.ring_stride;
         // ---------------- forward ----------------
         for (int l = 1; l <= L; ++l) {
-            const int nin = d.n[l - 1], nout = d.n[l], R = pl.rows[l], k0 = r * R;
-            const float* xin = (l == 1) ? x0 : smf + pl.x_off[l - 1] + par * pl.x_par;
-            const int xo = pl.x_off[l] + par * pl.x_par;
-            const int a = d.act[l - 1];
+            const int nin = sp.n[l - 1], nout = sp.n[l], R = sp.rows[l], k0 = r * R;
+            const float* xin = (l == 1) ? x0 : smf + sp.x_off[l - 1] + par * pl.x_par;
+            const int xo = sp.x_off[l] + par * pl.x_par;
+            const int a = sp.act[l - 1];
             const int own = max(0, min(R, nout - k0));
             if (tid == 0) mbar_arrive_expect_tx(&fbar[l][par], 4u * (uint32_t)(nout - own));
             const uint32_t fb = smem_u32(&fbar[l][par]);
@@ -221,9 +238,9 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
             for (int i = warp; i < R; i += kWarps) {
                 const int k = k0 + i;
                 if (k >= nout) break;
-                const float* w = smf + pl.w_off[l] + i * nin;
+                const float* w = smf + sp.w_off[l] + i * nin;
                 const float acc = warp_sum(xr.ok ? xr.dot(w, nin, lane) : dot_lanes(w, xin, nin, lane));
-                const float z = acc + smf[pl.b_off[l] + i];
+                const float z = acc + smf[sp.b_off[l] + i];
                 const float v = (a == PNN_SOFTMAX) ? z : act_fwd(a, z);
                 if (lane == r) smf[xo + k] = v;
                 else if (lane < C)                 // into peer `lane`'s x^l, completing its fbar
@@ -241,8 +258,8 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         }
         // ---------------- δ^L, own rows ----------------
         {
-            const int nL = d.n[L], R = pl.rows[L], k0 = r * R, aL = d.act[L - 1];
-            const float* xL = smf + pl.x_off[L] + par * pl.x_par;
+            const int nL = sp.n[L], R = sp.rows[L], k0 = r * R, aL = sp.act[L - 1];
+            const float* xL = smf + sp.x_off[L] + par * pl.x_par;
             for (int i = tid; i < R; i += kThreads) {
                 const int k = k0 + i;
                 float dl = 0.f;
@@ -250,15 +267,15 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
                     const float e = (k == label) ? 1.f : 0.f;
                     dl = (aL == PNN_SOFTMAX) ? xL[k] - e : (xL[k] - e) * act_deriv_from_x(aL, xL[k]);
                 }
-                smf[pl.d_off[L] + i] = dl;
+                smf[sp.d_off[L] + i] = dl;
             }
             __syncthreads();
         }
         // ---------------- δ^l, l = L-1..1: reduce-scatter of the partials ----------------
         for (int l = L - 1; l >= 1; --l) {
-            const int nl = d.n[l], Rn = pl.rows[l + 1], Rl = pl.rows[l];
-            const float* Wn = smf + pl.w_off[l + 1];          // own rows of W^{l+1}, pre-update (R6)
-            const float* dn = smf + pl.d_off[l + 1];
+            const int nl = sp.n[l], Rn = sp.rows[l + 1], Rl = sp.rows[l];
+            const float* Wn = smf + sp.w_off[l + 1];          // own rows of W^{l+1}, pre-update (R6)
+            const float* dn = smf + sp.d_off[l + 1];
             const int rv = pl.recv_off + par * pl.recv_par + l * pl.recv_layer;   // per layer: no reuse
                                                                                 // within a sample
             const int ownl = max(0, min(Rl, nl - r * Rl));
@@ -277,28 +294,28 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
             PROF(6);
             mbar_wait(&bbar[l][par], (uint32_t)((t >> 1) & 1));
             PROF(7);
-            const float* xl = smf + pl.x_off[l] + par * pl.x_par;
+            const float* xl = smf + sp.x_off[l] + par * pl.x_par;
             const int k0 = r * Rl;
             for (int i = tid; i < Rl; i += kThreads) {
                 float s = 0.f;
                 for (int src = 0; src < C; ++src) s += smf[rv + src * pl.recv_stride + i];
                 const int k = k0 + i;
-                smf[pl.d_off[l] + i] = (k < nl) ? s * act_deriv_from_x(d.act[l - 1], xl[k]) : 0.f;
+                smf[sp.d_off[l] + i] = (k < nl) ? s * act_deriv_from_x(sp.act[l - 1], xl[k]) : 0.f;
             }
             __syncthreads();
         }
         // ---------------- update (Eqs.12-13), own rows ----------------
         for (int l = 1; l <= L; ++l) {
-            const int nin = d.n[l - 1], nout = d.n[l], R = pl.rows[l], k0 = r * R;
-            const float* xin = (l == 1) ? x0 : smf + pl.x_off[l - 1] + par * pl.x_par;
+            const int nin = sp.n[l - 1], nout = sp.n[l], R = sp.rows[l], k0 = r * R;
+            const float* xin = (l == 1) ? x0 : smf + sp.x_off[l - 1] + par * pl.x_par;
             XRegs xr;
             xr.load(xin, nin, lane);
             for (int i = warp; i < R; i += kWarps) {
                 if (k0 + i >= nout) break;
-                const float g = lr * smf[pl.d_off[l] + i];
-                if (xr.ok) xr.axpy(smf + pl.w_off[l] + i * nin, -g, nin, lane);
-                else axpy_lanes(smf + pl.w_off[l] + i * nin, xin, -g, nin, lane);
-                if (lane == 0) smf[pl.b_off[l] + i] -= g;
+                const float g = lr * smf[sp.d_off[l] + i];
+                if (xr.ok) xr.axpy(smf + sp.w_off[l] + i * nin, -g, nin, lane);
+                else axpy_lanes(smf + sp.w_off[l] + i * nin, xin, -g, nin, lane);
+                if (lane == 0) smf[sp.b_off[l] + i] -= g;
             }
         }
         PROF(8);
