@@ -184,6 +184,21 @@ def test_cluster_kernel(orc, name, K, n, epochs):
     assert np.abs(merged - omerged).max() < TOL
 
 
+@pytest.mark.parametrize("kernel", ["resident", "cluster", "reference"])
+@pytest.mark.parametrize("rows_per_cn", [1, 2, 3, 4, 5, 6, 17])
+def test_short_slices(orc, kernel, rows_per_cn):
+    """Slices shorter than the resident kernel's lookahead / prefetch depths (L = 4,
+    8 rows in flight) and the cluster kernel's ring, with one ragged slice."""
+    c = CONFIGS["C4"]
+    K = 6
+    n = K * rows_per_cn + (1 if rows_per_cn > 1 else 0)
+    X, y = make_split(n, "train", 0)
+    _, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, 2, kernel)
+    okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=2)
+    assert np.abs(kids - okids).max() < TOL
+    assert np.abs(merged - omerged).max() < TOL
+
+
 def test_determinism_and_kernel_agreement(orc):
     c = CONFIGS["C4"]
     X, y = make_split(32 * 64, "train", 0)
