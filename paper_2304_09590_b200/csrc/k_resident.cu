@@ -761,6 +761,423 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     if constexpr (C > 1) cluster_sync_all();       // no CTA leaves while a peer may still st.async into it
 }
 
+// =====================================================================================
+// v10: the per-sample chain on a dedicated CTA.  A cluster of NSW + 1 CTAs trains one
+// CN: CTAs 0..NSW-1 hold U = ⌈H/NSW⌉ W¹ rows each in registers and only sweep (F, U as in
+// v8, same lookahead R27); CTA NSW runs the chain for all H units (4 warps, one unit per
+// lane: W², b1, b2 and the last L g's in registers).  Per sample the sweep CTAs send their
+// row-sum parts to the chain CTA (st.async → its aready mbarrier) and the chain sends
+// g(c) of each unit back to the owning sweep CTA (st.async → that CTA's gready).  The
+// chain never shares an SM sub-partition with a sweep, and the sweeps never run chain
+// code, so the period is max(sweep, chain) instead of their contended sum.
+#ifndef PNN_SPLIT_SAME_ORDER
+#define PNN_SPLIT_SAME_ORDER 0
+#endif
+// every sweep warp runs F then U (one code stream per SM sub-partition) instead of the
+// v8 phase shift (warps 4..7: U then F)
+constexpr bool kSplitSameOrder = PNN_SPLIT_SAME_ORDER != 0;
+constexpr int RS = 16;               // chain CTA: Gram-record ring slots
+constexpr int RPF = 8;               // records in flight
+constexpr int SPF = S - 2 * LAG - 1; // sweep CTAs: x prefetch distance (slot provably free, see below)
+static_assert(SPF >= 4, "x prefetch distance");
+
+struct __align__(16) SplitSmem {
+    uint64_t xfull[S];               // sweep: x(u) landed
+    uint64_t gready[GR];             // sweep: g(u) of the CTA's rows landed (from the chain CTA)
+    uint64_t aready[AR];             // chain: every sweep CTA's row-sum parts of sample c landed
+    uint64_t rfull[RS];              // chain: Gram record of sample c landed
+    float gbuf[GR][UMAX];            // sweep: g(u) of the CTA's rows
+    float asum[AR][2 * UMAX][4];     // chain: [c % AR][unit][part]
+    float zp[2][4][16];              // chain: [c & 1][warp][o] partial logits
+    float4 rec[RS][2];               // chain: Gram terms of sample c, label
+    float wx[NW][R][16];             // sweep: W¹ columns 768..783 of each warp's rows
+};
+constexpr size_t kSplitHead = ((sizeof(SplitSmem) + 127) / 128) * 128;
+
+template <int NSW, int A1, int A2>
+__global__ void __launch_bounds__(NW * 32, 1)
+sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ X,
+                 const float4* __restrict__ rec, long long n_local, int K_local, int s_first, float lr) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smraw);
+    float* xring = reinterpret_cast<float*>(smraw + kSplitHead);
+    const int D = d.n[0], H = d.n[1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int crank = (int)cluster_rank();          // 0..NSW-1 sweep CTAs, NSW the chain CTA
+    const int cn = s_first + (int)(blockIdx.x / (NSW + 1));
+    const int U = (H + NSW - 1) / NSW;               // units per sweep CTA
+    long long row0, T64;
+    shard_of(n_local, K_local, cn, &row0, &T64);
+    const int T = (int)T64;
+    float* P = children + (long long)cn * d.P;
+    float* W1 = P;
+    float* b1g = P + (long long)H * D;
+    float* W2 = b1g + H;
+    float* b2g = W2 + (long long)O * H;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
+        for (int i = 0; i < GR; ++i) mbar_init(&sm.gready[i], 1);
+        for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], 1);
+        for (int i = 0; i < RS; ++i) mbar_init(&sm.rfull[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    cluster_sync_all();                            // every CTA's barriers exist before any st.async
+
+    if (crank < NSW) {
+        // ================= sweep CTA =================
+        const int k0 = crank * U;
+        const int Uown = max(0, min(U, H - k0));
+        const float* Xc = X + row0 * (long long)D;
+        const uint32_t xbytes = (uint32_t)D * 4u;
+        auto issue_x = [&](int u) {
+            const int slot = u % S;
+            mbar_arrive_expect_tx(&sm.xfull[slot], xbytes);
+            bulk_g2s(xring + slot * DP, Xc + (long long)u * D, xbytes, &sm.xfull[slot]);
+        };
+        for (int i = threadIdx.x; i < S * DP; i += blockDim.x) xring[i] = 0.f;
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int u = 0; u < SPF && u < T; ++u) issue_x(u);
+        const int kr0 = warp * R;
+        uint64_t w[R][NP];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool live = kr0 + r < Uown;
+            const float* src = W1 + (long long)(k0 + kr0 + r) * D;
+#pragma unroll
+            for (int m = 0; m < NP; ++m)
+                w[r][m] = live ? *reinterpret_cast<const uint64_t*>(src + pcol(lane, m)) : 0ull;
+        }
+        const int tr = lane >> 2, tq = lane & 3;
+        const int nx = D - XC - 4 * tq;
+        const bool xlive = kr0 + tr < Uown;
+        float* wxp = &sm.wx[warp][tr][4 * tq];
+        {
+            float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float* src = W1 + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
+            if (xlive) {
+                if (nx > 0) w4.x = src[0];
+                if (nx > 1) w4.y = src[1];
+                if (nx > 2) w4.z = src[2];
+                if (nx > 3) w4.w = src[3];
+            }
+            *reinterpret_cast<float4*>(wxp) = w4;
+        }
+        __syncwarp();
+        // where this lane's row-sum part lands in the chain CTA, and that CTA's aready
+        const uint32_t apart = mapa(smem_u32(&sm.asum[0][k0 + kr0 + tr][tq]), (uint32_t)NSW);
+        const uint32_t abar = mapa(smem_u32(&sm.aready[0]), (uint32_t)NSW);
+        constexpr uint32_t kAStride = 2 * UMAX * 4 * 4;
+
+        auto sweep_f = [&](int s, int sx) {
+            mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));
+            const float* xn = xring + sx * DP + 4 * lane;
+            uint64_t acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = 0ull;
+            uint64_t xa, xb, ya, yb;                  // x quads q and q+1 in flight (2 ahead)
+            lds4(xn, xa, xb);
+            lds4(xn + 128, ya, yb);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t na = 0ull, nb = 0ull;
+                if (q + 2 < NQ) lds4(xn + 128 * (q + 2), na, nb);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
+                    acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
+                }
+                xa = ya; xb = yb;
+                ya = na; yb = nb;
+            }
+            float px;
+            {
+                const float4 w4 = *reinterpret_cast<const float4*>(wxp);
+                const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
+                px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
+            }
+            float v[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float lo, hi;
+                upk(acc[r], lo, hi);
+                v[r] = lo + hi;
+            }
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+            float u4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+            float u2[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
+            const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
+            const int a = s % AR;
+            st_async_f32_if(xlive, apart + (uint32_t)a * kAStride, part, abar + (uint32_t)a * 8u);
+        };
+#ifdef PNN_SPLIT_PROFILE
+        long long pw_g = 0, pw_tot0 = ptx::clock64();
+#endif
+        auto sweep_u = [&](int s, int sx) {
+            const int u = s - LAG;
+#ifdef PNN_SPLIT_PROFILE
+            const long long t0 = ptx::clock64();
+            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+            pw_g += ptx::clock64() - t0;
+#else
+            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+#endif
+            const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
+            const float* xo = xring + su * DP + 4 * lane;
+            const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
+            const float4 g0 = gv[0], g1 = gv[1];
+            const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
+            uint64_t xa, xb, ya, yb;
+            lds4(xo, xa, xb);
+            lds4(xo + 128, ya, yb);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t na = 0ull, nb = 0ull;
+                if (q + 2 < NQ) lds4(xo + 128 * (q + 2), na, nb);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
+                    w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
+                }
+                xa = ya; xb = yb;
+                ya = na; yb = nb;
+            }
+            float4 w4 = *reinterpret_cast<const float4*>(wxp);
+            const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
+            const float gq = -sm.gbuf[u % GR][kr0 + tr];
+            w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
+            w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
+            *reinterpret_cast<float4*>(wxp) = w4;
+        };
+
+        int sx = 0;                                // ring slot of x(s)
+        for (int s = 0; s < T + LAG; ++s) {
+            // g(s) of this CTA's rows will arrive from the chain CTA: post the expected bytes
+            if (threadIdx.x == 0 && s < T) mbar_arrive_expect_tx(&sm.gready[s % GR], 4u * (uint32_t)Uown);
+            const bool do_f = s < T, do_u = s >= LAG && s - LAG < T;
+            if (warp < 4 || kSplitSameOrder) {     // F before U (L correction terms in the chain)
+                if (do_f) sweep_f(s, sx);
+                if (do_u) sweep_u(s, sx);
+                // x(s+SPF) goes to the slot of x(s-2L-1), last read by U(s-L-1); every warp
+                // finished it before its F(s-L) parts reached the chain, i.e. before gready(s-L)
+                // (waited in U(s) just above) could complete
+                if (threadIdx.x == 0 && s + SPF < T) issue_x(s + SPF);   // (warp 0: F, U order)
+            } else {                               // U before F (one term fewer)
+                if (do_u) sweep_u(s, sx);
+                if (do_f) sweep_f(s, sx);
+            }
+            if (++sx == S) sx = 0;
+        }
+#ifdef PNN_SPLIT_PROFILE
+        if (blockIdx.x == 0 && lane == 0)
+            printf("sweep cta0 warp %d: T %d total %lld cyc/sample, gready wait %lld cyc/sample\n", warp, T,
+                   (ptx::clock64() - pw_tot0) / T, pw_g / T);
+#endif
+        float* W1o = opaque(W1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (kr0 + r < Uown) {
+                float* dst = W1o + (long long)(k0 + kr0 + r) * D;
+#pragma unroll
+                for (int m = 0; m < NP; ++m) *reinterpret_cast<uint64_t*>(dst + pcol(lane, m)) = w[r][m];
+            }
+        }
+        if (xlive) {
+            const float4 w4 = *reinterpret_cast<const float4*>(wxp);
+            float* dst = W1o + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
+            if (nx > 0) dst[0] = w4.x;
+            if (nx > 1) dst[1] = w4.y;
+            if (nx > 2) dst[2] = w4.z;
+            if (nx > 3) dst[3] = w4.w;
+        }
+    } else if (warp < 4) {
+        // ================= chain CTA: unit u = 32·warp + lane =================
+        const int u = 32 * warp + lane;
+        const bool lc = u < H;
+        const int sr = lc ? u / U : 0;             // owning sweep CTA and its row
+        const int r = u - sr * U;
+        const bool four = kSplitSameOrder || r < 32;   // rows of warps running F before U
+        float w2[O], b2[O];
+#pragma unroll
+        for (int o = 0; o < O; ++o) {
+            w2[o] = lc ? W2[(long long)o * H + u] : 0.f;
+            b2[o] = b2g[o];
+        }
+        float b1 = lc ? b1g[u] : 0.f;
+        float g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f;   // g(c-1) .. g(c-4) of this unit
+        const uint32_t gdst = mapa(smem_u32(&sm.gbuf[0][r]), (uint32_t)sr);
+        const uint32_t gbar = mapa(smem_u32(&sm.gready[0]), (uint32_t)sr);
+        const float4* Rc = rec + 2 * row0;
+        auto issue_rec = [&](int c) {
+            const int slot = c % RS;
+            mbar_arrive_expect_tx(&sm.rfull[slot], 32u);
+            bulk_g2s(&sm.rec[slot][0], Rc + 2 * c, 32u, &sm.rfull[slot]);
+        };
+        if (threadIdx.x == 0)
+            for (int c = 0; c < RPF && c < T; ++c) issue_rec(c);
+#ifdef PNN_SPLIT_PROFILE
+        long long pc_a = 0, pc_tot0 = ptx::clock64(), pc_tmp = 0;
+#endif
+        for (int c = 0; c < T; ++c) {
+            if (threadIdx.x == 0) {
+                mbar_arrive_expect_tx(&sm.aready[c % AR], 16u * (uint32_t)H);   // 4 parts of every unit
+                if (c + RPF < T) issue_rec(c + RPF);      // its slot held rec(c+RPF-RS): consumed
+            }
+            mbar_wait(&sm.rfull[c % RS], (uint32_t)((c / RS) & 1));
+            const float4 G = sm.rec[c % RS][0];
+            const int label = __float_as_int(sm.rec[c % RS][1].x);
+#ifdef PNN_SPLIT_PROFILE
+            pc_tmp = ptx::clock64();
+#endif
+            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
+#ifdef PNN_SPLIT_PROFILE
+            pc_a += ptx::clock64() - pc_tmp;
+#endif
+            // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c) (R27), h(c) ----
+            const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][u][0]);
+            float z = (pa.x + pa.y) + (pa.z + pa.w);
+            if (four) z = fmaf(-g4, G.x, z);
+            z = fmaf(-g3, G.y, z);
+            z = fmaf(-g2, G.z, z);
+            z = fmaf(-g1, G.w, z);
+            z += b1;
+            const float h = lc ? act_fwd_t<A1>(z) : 0.f;
+            // ---- this warp's partial logits: transpose-reduce over lanes ----
+            float pv0;
+            {
+                float pv[16];
+#pragma unroll
+                for (int o = 0; o < 16; ++o) pv[o] = (o < O) ? w2[o < O ? o : 0] * h : 0.f;
+                const bool c4 = lane & 16, c3 = lane & 8, c2 = lane & 4, c1 = lane & 2;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    pv[i] = (c4 ? pv[i + 8] : pv[i]) + __shfl_xor_sync(0xffffffffu, c4 ? pv[i] : pv[i + 8], 16);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    pv[i] = (c3 ? pv[i + 4] : pv[i]) + __shfl_xor_sync(0xffffffffu, c3 ? pv[i] : pv[i + 4], 8);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    pv[i] = (c2 ? pv[i + 2] : pv[i]) + __shfl_xor_sync(0xffffffffu, c2 ? pv[i] : pv[i + 2], 4);
+                pv0 = (c1 ? pv[1] : pv[0]) + __shfl_xor_sync(0xffffffffu, c1 ? pv[0] : pv[1], 2);
+                pv0 += __shfl_xor_sync(0xffffffffu, pv0, 1);
+            }
+            if ((lane & 1) == 0 && (lane >> 1) < O) sm.zp[c & 1][warp][lane >> 1] = pv0;
+            named_bar_sync(1, 128);                // the 4 warps' partials of sample c
+            // ---- δ2(c) in every lane ----
+            float dl[O];
+            {
+                float z2[O];
+#pragma unroll
+                for (int o = 0; o < O; ++o) z2[o] = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (i < (H + 31) / 32) {
+#pragma unroll
+                        for (int o = 0; o < O; ++o) z2[o] += sm.zp[c & 1][i][o];
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < O; ++o) z2[o] = b2[o] + z2[o];        // z2 = W2 h + b2 (Eq.2)
+                if constexpr (A2 == PNN_SOFTMAX) {
+                    const float m = fmaxf(fmaxf(fmaxf(z2[0], z2[1]), fmaxf(z2[2], z2[3])),
+                                          fmaxf(fmaxf(fmaxf(z2[4], z2[5]), fmaxf(z2[6], z2[7])), fmaxf(z2[8], z2[9])));
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = __expf(z2[o] - m);
+                    const float sum = ((dl[0] + dl[1]) + (dl[2] + dl[3])) +
+                                      (((dl[4] + dl[5]) + (dl[6] + dl[7])) + (dl[8] + dl[9]));
+                    float inv;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
+                } else {
+#pragma unroll
+                    for (int o = 0; o < O; ++o) {
+                        const float x2 = act_fwd_t<A2>(z2[o]);
+                        dl[o] = (x2 - ((o == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
+                    }
+                }
+            }
+            // ---- δ1, g(c) → the owning sweep CTA; W2, b1, b2 updates (registers) ----
+            float s1 = 0.f;                        // (W2ᵀδ2)_u with the pre-update W2 (R6)
+#pragma unroll
+            for (int o = 0; o < O; ++o) s1 = fmaf(w2[o], dl[o], s1);
+            const float gu = lc ? lr * (s1 * act_deriv_t<A1>(h)) : 0.f;
+            if (lc) st_async_f32(gdst + (uint32_t)(c % GR) * (uint32_t)(UMAX * 4), gu, gbar + (uint32_t)(c % GR) * 8u);
+            b1 -= gu;
+#pragma unroll
+            for (int o = 0; o < O; ++o) {
+                w2[o] = fmaf(-(lr * dl[o]), h, w2[o]);
+                b2[o] = fmaf(-lr, dl[o], b2[o]);
+            }
+            g4 = g3; g3 = g2; g2 = g1; g1 = gu;
+        }
+#ifdef PNN_SPLIT_PROFILE
+        if (blockIdx.x == NSW && lane == 0)
+            printf("chain warp %d: T %d total %lld cyc/sample, aready wait %lld cyc/sample\n", warp, T,
+                   (ptx::clock64() - pc_tot0) / T, pc_a / T);
+#endif
+        if (lc) {
+#pragma unroll
+            for (int o = 0; o < O; ++o) opaque(W2)[(long long)o * H + u] = w2[o];
+            opaque(b1g)[u] = b1;
+        }
+        if (u == 0) {
+#pragma unroll
+            for (int o = 0; o < O; ++o) opaque(b2g)[o] = b2[o];
+        }
+    }
+    cluster_sync_all();                            // no CTA leaves while a peer may still st.async into it
+}
+
+template <int NSW, int A1, int A2>
+cudaError_t launch_split_one(const ResidentPlan& p, const NetDesc& d, float* children, const float* x,
+                             const float4* rec, long long n_local, int K_local, int s_first, int s_count,
+                             float lr, cudaStream_t st) {
+    auto kern = sgd_split_kernel<NSW, A1, A2>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(s_count * (NSW + 1)));
+    cfg.blockDim = dim3((unsigned)p.threads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = NSW + 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, d, children, x, rec, n_local, K_local, s_first, lr);
+}
+
+template <int NSW>
+cudaError_t launch_split(const ResidentPlan& p, const NetDesc& d, float* children, const float* x,
+                         const float4* rec, long long n_local, int K_local, int s_first, int s_count,
+                         float lr, cudaStream_t st) {
+#define PNN_SPLIT_ACTS(A1_, A2_)                                                                   \
+    if (d.act[0] == A1_ && d.act[1] == A2_)                                                      \
+        return launch_split_one<NSW, A1_, A2_>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+    PNN_SPLIT_ACTS(PNN_RELU, PNN_SOFTMAX)
+    PNN_SPLIT_ACTS(PNN_TANH, PNN_SOFTMAX)
+    PNN_SPLIT_ACTS(PNN_SIGMOID, PNN_SOFTMAX)
+    PNN_SPLIT_ACTS(PNN_SIGMOID, PNN_SIGMOID)
+    PNN_SPLIT_ACTS(PNN_TANH, PNN_TANH)
+    PNN_SPLIT_ACTS(PNN_RELU, PNN_SIGMOID)
+    PNN_SPLIT_ACTS(PNN_LEAKY_RELU, PNN_SOFTMAX)
+#undef PNN_SPLIT_ACTS
+    return cudaErrorInvalidValue;
+}
+
 template <int C, int A1, int A2, bool TRACE>
 cudaError_t launch_one(const ResidentPlan& p, const NetDesc& d, float* children, const float* x,
                        const float4* rec, long long n_local, int K_local, int s_first, int s_count,
@@ -834,6 +1251,14 @@ ResidentPlan plan_resident(const NetDesc& d, int batch) {
     p.threads = NW * 32;                           // 8 warps; rows >= U are idle
     p.smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
     p.variant = 8;
+    // v10 (the chain on its own CTA) for H <= 128: 1 or 2 sweep CTAs + 1 chain CTA.  Opt-in
+    // (PNN_RESIDENT_V10=1): measured slower than v8 on C4
+    const char* v10 = getenv("PNN_RESIDENT_V10");
+    if (H <= 2 * UMAX && v10 && v10[0] == '1') {
+        p.variant = 10;
+        p.cluster = (H + UMAX - 1) / UMAX + 1;
+        p.smem = kSplitHead + sizeof(float) * (size_t)S * DP;
+    }
     p.ok = true;
     return p;
 }
@@ -845,6 +1270,11 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
     gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (p.variant == 10) {
+        if (p.cluster == 2) return launch_split<1>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+        if (p.cluster == 3) return launch_split<2>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+        return cudaErrorInvalidValue;
+    }
     switch (p.cluster) {
     case 1: return launch_c<1>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
     case 2: return launch_c<2>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);

@@ -199,6 +199,19 @@ def test_short_slices(orc, kernel, rows_per_cn):
     assert np.abs(merged - omerged).max() < TOL
 
 
+def test_resident_v10_split_variant(orc, monkeypatch):
+    """The opt-in v10 resident variant (chain on a dedicated CTA of a 3-CTA cluster;
+    PNN_RESIDENT_V10=1) on the C4 and C2 shapes with ragged and short slices."""
+    monkeypatch.setenv("PNN_RESIDENT_V10", "1")
+    for name, K, n in [("C4", 16, 16 * 70 + 5), ("C2", 4, 4 * 300 + 3), ("C4", 6, 6 * 3 + 1)]:
+        c = CONFIGS[name]
+        X, y = make_split(n, "train", 0)
+        _, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, 1, "resident")
+        okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, threads=8)
+        assert np.abs(kids - okids).max() < TOL, name
+        assert np.abs(merged - omerged).max() < TOL, name
+
+
 def test_determinism_and_kernel_agreement(orc):
     c = CONFIGS["C4"]
     X, y = make_split(32 * 64, "train", 0)
