@@ -37,8 +37,6 @@ namespace {
 
 constexpr int BMAX = 64;      // batch rows per step (one tile)
 constexpr int OMAX = 16;
-constexpr int FH = 16;        // fwd1: hidden units per CTA (× 64 batch rows; 256 threads, 1h × 4b each)
-constexpr int FK = 64;        // fwd1: k per smem stage
 constexpr int UT = 64;        // upd1: 64 h × 64 d per CTA (256 threads, 4 × 4 each)
 
 __device__ __forceinline__ long long batch_rows(long long n_local, int K_local, int z, int step, int B,
@@ -51,63 +49,69 @@ __device__ __forceinline__ long long batch_rows(long long n_local, int K_local, 
     return b;
 }
 
+// fwd1: a 64 (hidden) × 32 (batch) tile of Z1 per CTA, 256 threads × (4 h × 2 b), k-tiles of
+// 32 staged transposed in shared memory (W1 as [k][h], x as [k][b]) and prefetched into
+// registers one tile ahead: 8 FMA per 2 shared loads.
+constexpr int GH = 64, GB = 32, GK = 32;
 template <int A1>
 __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ children, const float* __restrict__ X,
                                                 float* __restrict__ A1buf, NetDesc d, long long n_local,
                                                 int K_local, int z0, int step, int B) {
-    __shared__ __align__(16) float ws[FH][FK + 1];
-    __shared__ __align__(16) float xs[FK][BMAX + 4];
-    const int z = z0 + blockIdx.y, h0 = blockIdx.x * FH;
+    __shared__ __align__(16) float ws[GK][GH + 4];
+    __shared__ __align__(16) float xs[GK][GB + 4];
+    const int z = z0 + blockIdx.z, h0 = blockIdx.x * GH, b0 = blockIdx.y * GB;
     const int D = d.n[0], H = d.n[1];
     long long row0;
     const long long bsz = batch_rows(n_local, K_local, z, step, B, &row0);
     const float* W1 = children + (long long)z * d.P + d.woff[1];
-    const int tid = threadIdx.x, th = tid >> 4, tb = (tid & 15) * 4;   // thread: hidden h0+th, rows tb..tb+3
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    // register-staged prefetch of the next k-tile while the current one is used
-    float wr[4];
-    float4 xr[4];
+    const int tid = threadIdx.x, hg = tid >> 4, bg = tid & 15;
+    float acc[4][2] = {};
+    // staging: W1 tile = 64 rows × 32 k = 512 float4-equivalents (2 per thread, as float2 pairs:
+    // the CN slab is only 8-byte aligned); x tile = 32 rows × 32 k = 256 float4 (1 per thread)
+    float2 wr[4];
+    float4 xr;
     auto load_tile = [&](int k0) {
-        const int r = tid >> 4, c = (tid & 15) * 4;
-        const int h = h0 + r, k = k0 + c;
-        const float* src = W1 + (long long)h * D + k;   // the CN slab need not be 16-B aligned
-        const bool ok = h < H && k < D;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) wr[i] = ok ? src[i] : 0.f;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int slot = tid + 256 * q;
-            const int b = slot >> 4, cc = (slot & 15) * 4, kk = k0 + cc;
-            xr[q] = (b < bsz && kk < D) ? *reinterpret_cast<const float4*>(X + (row0 + b) * D + kk)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < 2; ++q) {
+            const int slot = tid + 256 * q;                 // 0..511: row = slot >> 3, k = 4·(slot & 7)
+            const int r = slot >> 3, kk = k0 + 4 * (slot & 7);
+            const bool ok = h0 + r < H && kk < D;
+            const float2* src = reinterpret_cast<const float2*>(W1 + (long long)(h0 + r) * D + kk);
+            wr[2 * q] = ok ? src[0] : make_float2(0.f, 0.f);
+            wr[2 * q + 1] = ok ? src[1] : make_float2(0.f, 0.f);
+        }
+        {
+            const int r = tid >> 3, kk = k0 + 4 * (tid & 7);
+            const bool ok = b0 + r < bsz && kk < D;
+            xr = ok ? *reinterpret_cast<const float4*>(X + (row0 + b0 + r) * D + kk) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
     auto store_tile = [&]() {
-        const int r = tid >> 4, c = (tid & 15) * 4;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) ws[r][c + i] = wr[i];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
             const int slot = tid + 256 * q;
-            const int b = slot >> 4, cc = (slot & 15) * 4;
-            xs[cc][b] = xr[q].x; xs[cc + 1][b] = xr[q].y; xs[cc + 2][b] = xr[q].z; xs[cc + 3][b] = xr[q].w;
+            const int r = slot >> 3, kk = 4 * (slot & 7);
+            ws[kk][r] = wr[2 * q].x; ws[kk + 1][r] = wr[2 * q].y;
+            ws[kk + 2][r] = wr[2 * q + 1].x; ws[kk + 3][r] = wr[2 * q + 1].y;
         }
+        const int r = tid >> 3, kk = 4 * (tid & 7);
+        xs[kk][r] = xr.x; xs[kk + 1][r] = xr.y; xs[kk + 2][r] = xr.z; xs[kk + 3][r] = xr.w;
     };
     load_tile(0);
     store_tile();
     __syncthreads();
-    for (int k0 = 0; k0 < D; k0 += FK) {
-        const bool more = k0 + FK < D;
-        if (more) load_tile(k0 + FK);
-        const int kn = (D - k0) < FK ? (D - k0) : FK;
+    for (int k0 = 0; k0 < D; k0 += GK) {
+        const bool more = k0 + GK < D;
+        if (more) load_tile(k0 + GK);
+        const int kn = (D - k0) < GK ? (D - k0) : GK;
 #pragma unroll 8
         for (int k = 0; k < kn; ++k) {
-            const float w = ws[th][k];
-            const float4 xv = *reinterpret_cast<const float4*>(&xs[k][tb]);
-            acc[0] = fmaf(w, xv.x, acc[0]);
-            acc[1] = fmaf(w, xv.y, acc[1]);
-            acc[2] = fmaf(w, xv.z, acc[2]);
-            acc[3] = fmaf(w, xv.w, acc[3]);
+            const float4 w4 = *reinterpret_cast<const float4*>(&ws[k][4 * hg]);
+            const float2 x2 = *reinterpret_cast<const float2*>(&xs[k][2 * bg]);
+            acc[0][0] = fmaf(w4.x, x2.x, acc[0][0]); acc[0][1] = fmaf(w4.x, x2.y, acc[0][1]);
+            acc[1][0] = fmaf(w4.y, x2.x, acc[1][0]); acc[1][1] = fmaf(w4.y, x2.y, acc[1][1]);
+            acc[2][0] = fmaf(w4.z, x2.x, acc[2][0]); acc[2][1] = fmaf(w4.z, x2.y, acc[2][1]);
+            acc[3][0] = fmaf(w4.w, x2.x, acc[3][0]); acc[3][1] = fmaf(w4.w, x2.y, acc[3][1]);
         }
         __syncthreads();
         if (more) {
@@ -115,13 +119,16 @@ __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ childr
             __syncthreads();
         }
     }
-    const int h = h0 + th;
-    if (h < H) {
-        const float bias = children[(long long)z * d.P + d.woff[1] + (long long)H * D + h];
+    const float* b1 = children + (long long)z * d.P + d.woff[1] + (long long)H * D;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int b = b0 + 2 * bg + j;
+        if (b >= B) continue;
+        float* dst = A1buf + ((long long)z * BMAX + b) * H;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int b = tb + i;
-            if (b < B) A1buf[((long long)z * BMAX + b) * H + h] = (b < bsz) ? act_fwd_t<A1>(acc[i] + bias) : 0.f;
+            const int h = h0 + 4 * hg + i;
+            if (h < H) dst[h] = (b < bsz) ? act_fwd_t<A1>(acc[i][j] + b1[h]) : 0.f;
         }
     }
 }
@@ -301,8 +308,8 @@ template <int A1, int A2>
 cudaError_t enqueue_step(Mb32State* s, const NetDesc& d, float* children, const float* x, const int32_t* y,
                          long long n_local, int K_local, int z0, int zc, int step, float lr, cudaStream_t st) {
     const int H = d.n[1], D = d.n[0], B = s->B;
-    f32_fwd1<A1><<<dim3((unsigned)((H + FH - 1) / FH), (unsigned)zc), 256, 0, st>>>(children, x, s->A1, d, n_local,
-                                                                                    K_local, z0, step, B);
+    f32_fwd1<A1><<<dim3((unsigned)((H + GH - 1) / GH), (unsigned)((B + GB - 1) / GB), (unsigned)zc), 256, 0, st>>>(
+        children, x, s->A1, d, n_local, K_local, z0, step, B);
     f32_out<A2><<<dim3((unsigned)((B + 7) / 8), (unsigned)zc), 256, 0, st>>>(children, y, s->A1, s->D2, d, n_local,
                                                                              K_local, z0, step, B);
     f32_hid<A1><<<dim3((unsigned)((H + 63) / 64), (unsigned)zc), 256, 0, st>>>(children, s->A1, s->D2, s->D1, d,
