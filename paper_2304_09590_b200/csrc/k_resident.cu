@@ -873,7 +873,9 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
         constexpr uint32_t kAStride = 2 * UMAX * 4 * 4;
 
         auto sweep_f = [&](int s, int sx) {
+#ifndef PNN_EXP_SW_NOXWAIT
             mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));
+#endif
             const float* xn = xring + sx * DP + 4 * lane;
             uint64_t acc[R];
 #pragma unroll
@@ -893,12 +895,14 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 xa = ya; xb = yb;
                 ya = na; yb = nb;
             }
-            float px;
+            float px = 0.f;
+#ifndef PNN_EXP_SW_NOWX
             {
                 const float4 w4 = *reinterpret_cast<const float4*>(wxp);
                 const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
                 px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
             }
+#endif
             float v[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -906,6 +910,9 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 upk(acc[r], lo, hi);
                 v[r] = lo + hi;
             }
+#ifdef PNN_EXP_SW_NORED
+            const float part = v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7] + px;
+#else
             const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
             float u4[4];
 #pragma unroll
@@ -916,6 +923,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             for (int i = 0; i < 2; ++i)
                 u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
             const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
+#endif
             const int a = s % AR;
             st_async_f32_if(xlive, apart + (uint32_t)a * kAStride, part, abar + (uint32_t)a * 8u);
         };
@@ -926,10 +934,12 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             const int u = s - LAG;
 #ifdef PNN_SPLIT_PROFILE
             const long long t0 = ptx::clock64();
+#endif
+#ifndef PNN_EXP_SW_NOGWAIT
             mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+#endif
+#ifdef PNN_SPLIT_PROFILE
             pw_g += ptx::clock64() - t0;
-#else
-            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
 #endif
             const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
             const float* xo = xring + su * DP + 4 * lane;
@@ -951,12 +961,14 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 xa = ya; xb = yb;
                 ya = na; yb = nb;
             }
+#ifndef PNN_EXP_SW_NOWX
             float4 w4 = *reinterpret_cast<const float4*>(wxp);
             const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
             const float gq = -sm.gbuf[u % GR][kr0 + tr];
             w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
             w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
             *reinterpret_cast<float4*>(wxp) = w4;
+#endif
         };
 
         int sx = 0;                                // ring slot of x(s)
