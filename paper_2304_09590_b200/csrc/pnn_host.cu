@@ -414,8 +414,20 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         net->stage_rows = n;
     }
     // Pipeline: the CNs are cut into groups; group g's slices are copied on
-    // copy_stream while group g-1 trains on the caller's stream.
-    const int groups = net->K_local >= 8 ? 8 : net->K_local;
+    // copy_stream while group g-1 trains on the caller's stream.  A group must still fill
+    // the GPU: the batched mini-batch paths take every CN at once (one group), the cluster
+    // kernels run ~148/cluster CNs concurrently.
+    int groups = 1;
+    {
+        ResidentPlan rp{};
+        const int k = choose_kernel(net, &rp);
+        int cap = net->K_local;                   // CNs that run concurrently
+        if (k == PNN_KERNEL_RESIDENT) cap = 148 / (rp.cluster > 0 ? rp.cluster : 1);
+        else if (k == PNN_KERNEL_CLUSTER) cap = 148 / plan_cluster(net->d, net->batch).cluster;
+        else if (k == PNN_KERNEL_REFERENCE) cap = 148;
+        groups = net->K_local / (cap > 0 ? cap : 1);
+        groups = groups < 1 ? 1 : (groups > 8 ? 8 : groups);
+    }
     const size_t row_bytes = sizeof(float) * net->d.n[0];
     cudaEvent_t ready[8];
     for (int g = 0; g < groups; ++g) CUDA_TRY(net, cudaEventCreateWithFlags(&ready[g], cudaEventDisableTiming));
