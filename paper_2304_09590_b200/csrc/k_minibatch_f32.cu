@@ -271,6 +271,18 @@ __global__ void __launch_bounds__(256) f32_upd1(float* __restrict__ children, co
     long long row0;
     const long long bsz = batch_rows(n_local, K_local, z, step, B, &row0);
     if (bsz == 0) return;
+    // this thread's 4 × 4 W1 values, loaded first so their latency overlaps the staging and
+    // the product (scalar: the CN slab need not be 16-B aligned)
+    const int th = (threadIdx.x >> 4) * 4, tdd = (threadIdx.x & 15) * 4;
+    float* W1 = children + (long long)z * d.P + d.woff[1];
+    float wold[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int h = h0 + th + i, dd = d0 + tdd + j;
+            wold[i][j] = (h < H && dd < D) ? W1[(long long)h * D + dd] : 0.f;
+        }
     for (int slot = threadIdx.x; slot < (int)bsz * (UT / 4); slot += blockDim.x) {
         const int b = slot / (UT / 4), c = (slot % (UT / 4)) * 4;
         float4 dv = make_float4(0.f, 0.f, 0.f, 0.f), xv = dv;
@@ -280,7 +292,6 @@ __global__ void __launch_bounds__(256) f32_upd1(float* __restrict__ children, co
         *reinterpret_cast<float4*>(&xs[b][c]) = xv;
     }
     __syncthreads();
-    const int th = (threadIdx.x >> 4) * 4, tdd = (threadIdx.x & 15) * 4;
     float acc[4][4] = {};
     for (int b = 0; b < (int)bsz; ++b) {
         const float4 dv = *reinterpret_cast<const float4*>(&ds[b][th]);
@@ -291,16 +302,15 @@ __global__ void __launch_bounds__(256) f32_upd1(float* __restrict__ children, co
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(dd[i], xx[j], acc[i][j]);
     }
-    float* W1 = children + (long long)z * d.P + d.woff[1];
     const float fb = (float)bsz;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int h = h0 + th + i;
         if (h >= H) continue;
-        float* w = W1 + (long long)h * D + d0 + tdd;   // scalar: the slab need not be 16-B aligned
+        float* w = W1 + (long long)h * D + d0 + tdd;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (d0 + tdd + j < D) w[j] -= lr * (acc[i][j] / fb);
+            if (d0 + tdd + j < D) w[j] = wold[i][j] - lr * (acc[i][j] / fb);
     }
 }
 
