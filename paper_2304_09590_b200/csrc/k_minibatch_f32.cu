@@ -138,13 +138,16 @@ template <int A2>
 __global__ void __launch_bounds__(256) f32_out(const float* __restrict__ children, const int32_t* __restrict__ Y,
                                                const float* __restrict__ A1buf, float* __restrict__ D2buf,
                                                NetDesc d, long long n_local, int K_local, int z0, int step, int B) {
+    extern __shared__ float w2s[];                 // [O][H]: W2 staged once per CTA
     const int z = z0 + blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = d.n[1], O = d.n[2];
+    const float* W2 = children + (long long)z * d.P + d.woff[2];
+    for (int i = threadIdx.x; i < O * H; i += blockDim.x) w2s[i] = W2[i];
+    __syncthreads();
     const int b = blockIdx.x * 8 + warp;
     if (b >= B) return;
-    const int H = d.n[1], O = d.n[2];
     long long row0;
     const long long bsz = batch_rows(n_local, K_local, z, step, B, &row0);
-    const float* W2 = children + (long long)z * d.P + d.woff[2];
     const float* b2 = W2 + (long long)O * H;
     const float* a1 = A1buf + ((long long)z * BMAX + b) * H;
     float acc[OMAX];
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(256) f32_out(const float* __restrict__ childre
         const float a = a1[h];
 #pragma unroll
         for (int o = 0; o < OMAX; ++o)
-            if (o < O) acc[o] = fmaf(W2[(long long)o * H + h], a, acc[o]);
+            if (o < O) acc[o] = fmaf(w2s[o * H + h], a, acc[o]);
     }
 #pragma unroll
     for (int o = 0; o < OMAX; ++o) acc[o] = warp_sum(acc[o]);
@@ -320,8 +323,8 @@ cudaError_t enqueue_step(Mb32State* s, const NetDesc& d, float* children, const 
     const int H = d.n[1], D = d.n[0], B = s->B;
     f32_fwd1<A1><<<dim3((unsigned)((H + GH - 1) / GH), (unsigned)((B + GB - 1) / GB), (unsigned)zc), 256, 0, st>>>(
         children, x, s->A1, d, n_local, K_local, z0, step, B);
-    f32_out<A2><<<dim3((unsigned)((B + 7) / 8), (unsigned)zc), 256, 0, st>>>(children, y, s->A1, s->D2, d, n_local,
-                                                                             K_local, z0, step, B);
+    f32_out<A2><<<dim3((unsigned)((B + 7) / 8), (unsigned)zc), 256, sizeof(float) * (size_t)d.n[2] * H, st>>>(
+        children, y, s->A1, s->D2, d, n_local, K_local, z0, step, B);
     f32_hid<A1><<<dim3((unsigned)((H + 63) / 64), (unsigned)zc), 256, 0, st>>>(children, s->A1, s->D2, s->D1, d,
                                                                                n_local, K_local, z0, step, B, lr);
     f32_upd1<<<dim3((unsigned)((H + UT - 1) / UT), (unsigned)((D + UT - 1) / UT), (unsigned)zc), 256, 0, st>>>(
@@ -364,6 +367,7 @@ const char* mb32_plan(const NetDesc& d, int batch) {
     if (d.n[0] % 4 != 0) return "inputs must be a multiple of 4 (16-byte rows)";
     if (d.n[1] % 4 != 0) return "hidden width must be a multiple of 4";
     if (d.n[2] > OMAX) return "at most 16 outputs";
+    if ((size_t)d.n[2] * d.n[1] * sizeof(float) > 48 * 1024) return "W2 (outputs × hidden) must fit 48 KB of shared memory";
     const int a1 = d.act[0], a2 = d.act[1];
     const bool built = (a2 == PNN_SOFTMAX && (a1 == PNN_RELU || a1 == PNN_LEAKY_RELU || a1 == PNN_TANH ||
                                               a1 == PNN_SIGMOID)) ||
