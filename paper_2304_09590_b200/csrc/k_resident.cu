@@ -69,6 +69,11 @@ constexpr int CMAX = 4;       // cluster size
 #ifndef PNN_EXP_CHAIN_PAIRS
 #define PNN_EXP_CHAIN_PAIRS 4
 #endif
+#ifndef PNN_V8_SAME_ORDER
+#define PNN_V8_SAME_ORDER 0
+#endif
+// every warp runs F then U (instead of warps 4..7 running U before F)
+constexpr bool kV8SameOrder = PNN_V8_SAME_ORDER != 0;
 #ifndef PNN_CHAIN_V9
 #define PNN_CHAIN_V9 0
 #endif
@@ -327,7 +332,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         // warps 4..7 (the sub-partition partners of warps 0..3) run U before F: the two sweeps
         // of a sub-partition are then out of phase, and those rows' F(s) sees g(s-L) already
         // applied (one correction term fewer in the chain)
-        if (warp < 4) {
+        if (warp < 4 || kV8SameOrder) {
         if (s < T) {
             // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
 #if PNN_SWEEP_XWAIT
@@ -538,7 +543,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             const int label = __float_as_int(xring[cs * DP + GOFF + 4]);
             const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][uc][0]);
             float z = (pa.x + pa.y) + (pa.z + pa.w);
-            if (half == 0) z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);   // rows of warps 0..3
+            if (half == 0 || kV8SameOrder) z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);   // F-before-U rows
             z = fmaf(-sm.gbuf[(c + GR - 3) % GR][uc], G.y, z);
             z = fmaf(-sm.gbuf[(c + GR - 2) % GR][uc], G.z, z);
             z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
