@@ -18,6 +18,11 @@ NOISE_SIGMA = 0.1               # "N(0,0.1)" read as sigma = 0.1 (SURVEY.md §8c
 BLOB_SIGMA = 1.5
 N_BLOBS = 12
 _SPLIT_ID = {"train": 0, "test": 1}
+# "hard" variant for the §8(f) accuracy experiments only (the parity tests and benches use the
+# default recipe): each image blends its prototype with another class's, x = (1-a)·P_y + a·P_y2
+# + 0.35·N(0,1), a ~ U(0, 0.5), drawn from a separate stream so the default bytes are unchanged
+HARD_SIGMA = 0.35
+HARD_BLEND = 0.5
 
 
 @functools.lru_cache(maxsize=8)
@@ -43,7 +48,17 @@ def prototypes(seed: int = 0) -> np.ndarray:
     return protos
 
 
-def _chunk(seed: int, split: int, c: int, protos: np.ndarray):
+def _chunk(seed: int, split: int, c: int, protos: np.ndarray, hard: bool = False):
+    if hard:
+        rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, split, c, 1])))
+        y = rng.integers(0, N_CLASSES, size=CHUNK, dtype=np.int32)
+        y2 = (y + rng.integers(1, N_CLASSES, size=CHUNK, dtype=np.int32)) % N_CLASSES
+        a = rng.uniform(0.0, HARD_BLEND, size=(CHUNK, 1)).astype(np.float32)
+        x = rng.standard_normal((CHUNK, N_PIXELS), dtype=np.float32)
+        x *= np.float32(HARD_SIGMA)
+        x += (1.0 - a) * protos[y] + a * protos[y2]
+        np.clip(x, 0.0, 1.0, out=x)
+        return x, y
     rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, split, c])))
     y = rng.integers(0, N_CLASSES, size=CHUNK, dtype=np.int32)
     x = rng.standard_normal((CHUNK, N_PIXELS), dtype=np.float32)
@@ -54,7 +69,7 @@ def _chunk(seed: int, split: int, c: int, protos: np.ndarray):
 
 
 def make_rows(start: int, n: int, split: str = "train", seed: int = 0,
-              out_x: np.ndarray | None = None, out_y: np.ndarray | None = None):
+              out_x: np.ndarray | None = None, out_y: np.ndarray | None = None, hard: bool = False):
     """Rows [start, start+n) of a split: (X [n,784] float32, y [n] int32).
 
     Row r is always the same bytes regardless of which range asked for it.
@@ -68,7 +83,7 @@ def make_rows(start: int, n: int, split: str = "train", seed: int = 0,
     c0, c1 = start // CHUNK, (start + n - 1) // CHUNK
 
     def fill(c):
-        cx, cy = _chunk(seed, sid, c, protos)
+        cx, cy = _chunk(seed, sid, c, protos, hard)
         lo = max(start, c * CHUNK)
         hi = min(start + n, (c + 1) * CHUNK)
         x[lo - start:hi - start] = cx[lo - c * CHUNK:hi - c * CHUNK]
@@ -84,6 +99,6 @@ def make_rows(start: int, n: int, split: str = "train", seed: int = 0,
     return x, y
 
 
-def make_split(n: int, split: str = "train", seed: int = 0):
+def make_split(n: int, split: str = "train", seed: int = 0, hard: bool = False):
     """The first n rows of a split."""
-    return make_rows(0, n, split, seed)
+    return make_rows(0, n, split, seed, hard=hard)

@@ -46,6 +46,9 @@ def _timed(fn):
     return a.elapsed_time(b)
 
 
+DATA = "hard"
+
+
 def run_curves(cfg, K, epochs, data, act=None, lr=None, tag="curves"):
     xd, yd, xt, yt = data
     net = _net(cfg, K, act, lr)
@@ -54,7 +57,7 @@ def run_curves(cfg, K, epochs, data, act=None, lr=None, tag="curves"):
         net.merge()
         acc, conf, cost = net.evaluate(xt, yt)
         cn = np.array([net.evaluate(xt, yt, subnet=i) for i in range(K)])
-        print(json.dumps({"exp": tag, "config": cfg.name, "act": act or list(cfg.act), "K": K,
+        print(json.dumps({"exp": tag, "config": cfg.name, "data": DATA, "act": act or list(cfg.act), "K": K,
                           "lr": lr or cfg.lr, "batch": cfg.batch, "epoch": e, "train_ms": ms,
                           "pnn": {"accuracy": acc, "confidence": conf, "cost": cost},
                           "cn_mean": {"accuracy": float(cn[:, 0].mean()), "confidence": float(cn[:, 1].mean()),
@@ -72,14 +75,18 @@ def main():
     ap.add_argument("--lr", type=float, default=None)
     ap.add_argument("--slots", default="1,2,4,8,16,32,64")
     ap.add_argument("--rows", type=int, default=None, help="override the training rows")
+    ap.add_argument("--data", default="hard", choices=["hard", "easy"],
+                    help="hard: the blended/noisier datagen variant (the default recipe is ~100%% separable)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
+    global DATA
+    DATA = args.data
 
     if args.what in ("curves", "sweep"):
         cfg = CONFIGS[args.config or "F1"]
         n = args.rows or cfg.n_train
-        X, y = make_split(n, "train", 0)
-        Xt, yt = make_split(cfg.n_test, "test", 0)
+        X, y = make_split(n, "train", 0, hard=args.data == "hard")
+        Xt, yt = make_split(cfg.n_test, "test", 0, hard=args.data == "hard")
         data = (torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(),
                 torch.from_numpy(Xt).cuda(), torch.from_numpy(yt).cuda())
         epochs = args.epochs or cfg.epochs
