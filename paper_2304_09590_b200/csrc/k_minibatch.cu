@@ -60,7 +60,7 @@ static cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int
         }
     }
     dim3 grid((unsigned)((M + tc::BM - 1) / tc::BM), (unsigned)((N + BN - 1) / BN), (unsigned)Z);
-    kern<<<grid, 128, smem, st>>>(ta, tb, K, ep);
+    kern<<<grid, tc::threads_for(BN), smem, st>>>(ta, tb, K, ep);
     return cudaGetLastError();
 }
 
@@ -110,8 +110,11 @@ struct MbState {
     long long P, woff1, woff2, woff3;
     __nv_bfloat16 *W1b, *W2b, *W2bT, *W3b, *Xs, *XsT, *A1, *A1T, *A2, *d2b, *d2bT, *d1T, *d3b;
     __nv_bfloat16* W2bT2;     // second W2ᵀ copy: step j's B4 reads [j & 1] while B3 writes the other
+    __nv_bfloat16 *Xs2, *XsT2;  // second input copy: step j+1's cast runs beside step j's tail
     float* d3;
-    CUtensorMap tW1b, tXs, tW2b, tA1, tW2bT, td2b, td2bT, tA1T, td1T, tXsT, tW2bT2;
+    CUtensorMap tW1b, tXs, tW2b, tA1, tW2bT, td2b, td2bT, tA1T, td1T, tXsT, tW2bT2, tXs2, tXsT2;
+    cudaStream_t cxs = nullptr;           // the next step's input cast (forked inside the graph)
+    cudaEvent_t ev_go = nullptr, ev_cx = nullptr;
     cudaStream_t side = nullptr;          // B3 runs beside B4 -> B5 (forked inside the graph)
     cudaEvent_t ev_ob = nullptr, ev_b3 = nullptr;
     // the epoch's launch sequence as a CUDA graph, re-used while its arguments are unchanged
@@ -155,7 +158,7 @@ const char* mb_plan(const NetDesc& d, int batch) {
 
 void mb_destroy(MbState* s) {
     if (!s) return;
-    __nv_bfloat16* bufs[] = {s->W2bT2, s->W1b, s->W2b, s->W2bT, s->W3b, s->Xs, s->XsT, s->A1, s->A1T, s->A2, s->d2b,
+    __nv_bfloat16* bufs[] = {s->Xs2, s->XsT2, s->W2bT2, s->W1b, s->W2b, s->W2bT, s->W3b, s->Xs, s->XsT, s->A1, s->A1T, s->A2, s->d2b,
                              s->d2bT, s->d1T, s->d3b};
     for (auto* b : bufs) cudaFree(b);
     cudaFree(s->d3);
@@ -163,6 +166,9 @@ void mb_destroy(MbState* s) {
         if (e.exec) cudaGraphExecDestroy(e.exec);
     if (s->cap) cudaStreamDestroy(s->cap);
     if (s->side) cudaStreamDestroy(s->side);
+    if (s->cxs) cudaStreamDestroy(s->cxs);
+    if (s->ev_go) cudaEventDestroy(s->ev_go);
+    if (s->ev_cx) cudaEventDestroy(s->ev_cx);
     if (s->ev_ob) cudaEventDestroy(s->ev_ob);
     if (s->ev_b3) cudaEventDestroy(s->ev_b3);
     delete s;
@@ -176,7 +182,7 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     const long long Z = K_local, D = s->D, H1 = s->H1, H2 = s->H2, B = s->B;
     struct { __nv_bfloat16** p; long long n; } al[] = {
         {&s->W1b, Z * H1 * D}, {&s->W2b, Z * H2 * H1}, {&s->W2bT, Z * H1 * H2}, {&s->W2bT2, Z * H1 * H2}, {&s->W3b, Z * 16 * H2},
-        {&s->Xs, Z * B * D}, {&s->XsT, Z * D * B}, {&s->A1, Z * B * H1}, {&s->A1T, Z * H1 * B},
+        {&s->Xs, Z * B * D}, {&s->XsT, Z * D * B}, {&s->Xs2, Z * B * D}, {&s->XsT2, Z * D * B}, {&s->A1, Z * B * H1}, {&s->A1T, Z * H1 * B},
         {&s->A2, Z * B * H2}, {&s->d2b, Z * B * H2}, {&s->d2bT, Z * H2 * B}, {&s->d1T, Z * H1 * B},
         {&s->d3b, Z * B * 16}};
     *err = cudaSuccess;
@@ -186,6 +192,9 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     if (*err == cudaSuccess) *err = cudaMemset(s->W3b, 0, sizeof(__nv_bfloat16) * (size_t)(Z * 16 * H2));
     if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+    if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->cxs, cudaStreamNonBlocking);
+    if (*err == cudaSuccess) *err = cudaEventCreateWithFlags(&s->ev_go, cudaEventDisableTiming);
+    if (*err == cudaSuccess) *err = cudaEventCreateWithFlags(&s->ev_cx, cudaEventDisableTiming);
     if (*err == cudaSuccess) *err = cudaEventCreateWithFlags(&s->ev_ob, cudaEventDisableTiming);
     if (*err == cudaSuccess) *err = cudaEventCreateWithFlags(&s->ev_b3, cudaEventDisableTiming);
     if (*err == cudaSuccess) *err = prepare_gemm_attrs();
@@ -202,6 +211,8 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     ok = ok && make_tmap_kmajor(&s->tA1T, s->A1T, (int)B, (int)H1, iZ, 256);
     ok = ok && make_tmap_kmajor(&s->td1T, s->d1T, (int)B, (int)H1, iZ, tc::BM);
     ok = ok && make_tmap_kmajor(&s->tXsT, s->XsT, (int)B, (int)D, iZ, 256);
+    ok = ok && make_tmap_kmajor(&s->tXs2, s->Xs2, (int)D, (int)B, iZ, (int)B);
+    ok = ok && make_tmap_kmajor(&s->tXsT2, s->XsT2, (int)B, (int)D, iZ, 256);
     if (!ok) {
         if (*err == cudaSuccess) *err = cudaErrorInvalidValue;
         mb_destroy(s);
@@ -249,8 +260,9 @@ __global__ void mb_cast_w(const float* __restrict__ children, MbState s, int z0,
 // Xs[z][b][d] = bf16(x[row]) and XsT[z][d][b], row = start(z) + step·B + b (0 past the
 // slice); one CTA per 64-column chunk of d and CN, transposed through shared memory so
 // that both stores are coalesced.
-__global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, MbState s, long long n_local,
-                                                 int K_local, int z0, int step) {
+__global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, MbState s, __nv_bfloat16* __restrict__ xs,
+                                                 __nv_bfloat16* __restrict__ xst, long long n_local, int K_local,
+                                                 int z0, int step) {
     __shared__ __nv_bfloat16 t[64][66];
     const int z = z0 + blockIdx.y, d0 = blockIdx.x * 64;
     long long st;
@@ -261,14 +273,14 @@ __global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, Mb
         const long long tr = (long long)step * s.B + b;
         if (b < s.B && dd < w) {
             const __nv_bfloat16 v = __float2bfloat16_rn(tr < cnt ? X[(st + tr) * s.D + d0 + dd] : 0.f);
-            s.Xs[((long long)z * s.B + b) * s.D + d0 + dd] = v;
+            xs[((long long)z * s.B + b) * s.D + d0 + dd] = v;
             t[b][dd] = v;
         }
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
         const int dd = idx >> 6, b = idx & 63;
-        if (b < s.B && dd < w) s.XsT[((long long)z * s.D + d0 + dd) * s.B + b] = t[b][dd];
+        if (b < s.B && dd < w) xst[((long long)z * s.D + d0 + dd) * s.B + b] = t[b][dd];
     }
 }
 
@@ -436,14 +448,29 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         base.step = (int)j;
         // B3 of step j-1 (side stream) still reads A1T / δ2bT and writes W2b: join before F1(j)
         if (j > 0 && (e = cudaStreamWaitEvent(st, s->ev_b3, 0))) return e;
-        mb_cast_x<<<dim3((unsigned)((s->D + 63) / 64), (unsigned)s_count), 256, 0, st>>>(x, *s, n_local, K_local,
-                                                                                      s_first, (int)j);
+        const bool odd_x = (j & 1) != 0;
+        const dim3 cgrid((unsigned)((s->D + 63) / 64), (unsigned)s_count);
+        if (j == 0) {
+            mb_cast_x<<<cgrid, 256, 0, st>>>(x, *s, s->Xs, s->XsT, n_local, K_local, s_first, 0);
+        } else if ((e = cudaStreamWaitEvent(st, s->ev_cx, 0))) {   // this step's input cast (forked)
+            return e;
+        }
         // F1: A1 = relu(W1b·Xsᵀ + b1)
         tc::Epi f1 = base;
         f1.M = s->H1; f1.N = B; f1.nvalid = B;
         f1.bias = children + s->woff1 + (long long)s->H1 * s->D; f1.zs_bias = s->P;
         f1.out_bm = s->A1; f1.out_mb = s->A1T; f1.zs_act = (long long)s->H1 * B;
-        if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW1b, s->tXs, s_count, s->H1, B, s->D, f1, st))) return e;
+        if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW1b, odd_x ? s->tXs2 : s->tXs, s_count, s->H1, B, s->D, f1, st)))
+            return e;
+        // the next step's input cast runs beside this step's tail: its buffer was last read by
+        // this buffer parity's F1 and B5 of step j-1, both before F1(j) on this stream
+        if (j + 1 < steps) {
+            if ((e = cudaEventRecord(s->ev_go, st))) return e;
+            if ((e = cudaStreamWaitEvent(s->cxs, s->ev_go, 0))) return e;
+            mb_cast_x<<<cgrid, 256, 0, s->cxs>>>(x, *s, odd_x ? s->Xs : s->Xs2, odd_x ? s->XsT : s->XsT2, n_local,
+                                                  K_local, s_first, (int)j + 1);
+            if ((e = cudaEventRecord(s->ev_cx, s->cxs))) return e;
+        }
         // F2: A2 = relu(W2b·A1ᵀ + b2)
         tc::Epi f2 = base;
         f2.M = s->H2; f2.N = B; f2.nvalid = B;
@@ -478,7 +505,8 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         b5.M = s->H1; b5.N = s->D; b5.nvalid = s->D;
         b5.master = children + s->woff1; b5.zs_master = s->P;
         b5.wb = s->W1b; b5.wbt = nullptr; b5.zs_w = (long long)s->H1 * s->D;
-        if ((e = launch_gemm<256, tc::EPI_UPD>(s->td1T, s->tXsT, s_count, s->H1, s->D, B, b5, st))) return e;
+        if ((e = launch_gemm<256, tc::EPI_UPD>(s->td1T, odd_x ? s->tXsT2 : s->tXsT, s_count, s->H1, s->D, B, b5, st)))
+            return e;
     }
     if (steps > 0 && (e = cudaStreamWaitEvent(st, s->ev_b3, 0))) return e;   // join the side stream
     return cudaGetLastError();

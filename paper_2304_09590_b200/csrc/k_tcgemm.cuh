@@ -25,6 +25,9 @@ constexpr int BM = 128;       // tile rows (UMMA M)
 constexpr int BK = 64;        // K per stage: 64 bf16 = one 128-byte swizzle row
 // pipeline depth: 8 stages for the narrow tiles (long K: more TMA loads in flight), 2 for BN = 256 (the update GEMMs
 // have K = 64, a single stage) so that two CTAs fit per SM
+// threads per CTA: the wide update tiles (BN = 256, memory-bound epilogues) use 8 warps, two
+// per TMEM lane quadrant, each taking half of the columns
+__host__ __device__ constexpr int threads_for(int bn) { return bn >= 256 ? 256 : 128; }
 __host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? 2 : (bn >= 128 ? 4 : 8); }
 
 enum { EPI_STORE_F32 = 0, EPI_FWD = 1, EPI_BWD = 2, EPI_UPD = 3 };
@@ -166,7 +169,7 @@ struct __align__(1024) GemmSmem {
 };
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(threads_for(BN))
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, Epi ep) {
     extern __shared__ __align__(1024) unsigned char raw[];
     GemmSmem<BN>& s = *reinterpret_cast<GemmSmem<BN>*>(
@@ -175,7 +178,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, z = blockIdx.z + ep.zoff;
     const int nk = (K + BK - 1) / BK;
     constexpr int STAGES = GemmSmem<BN>::STAGES;
-    static_assert(sizeof(GemmSmem<BN>::a) >= 4 * 32 * 33 * sizeof(float), "epilogue tile");
+    constexpr int NWE = threads_for(BN) / 32;     // epilogue warps: 4, or 8 (two per lane quadrant)
+    constexpr int CSPAN = BN / (NWE / 4);          // columns per epilogue warp
+    static_assert(sizeof(GemmSmem<BN>::a) + sizeof(GemmSmem<BN>::b) >= NWE * 32 * 33 * sizeof(float),
+                  "epilogue tiles");
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
@@ -226,17 +232,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     mbar_wait(&s.accf, 0u);
     __syncwarp();
     fence_after();
-    float (*tile)[33] = reinterpret_cast<float (*)[33]>(&s.a[0][0]) + 32 * warp;
-    const int mrow0 = m0 + 32 * warp;
+    float (*tile)[33] = reinterpret_cast<float (*)[33]>(&s.a[0][0]) + 32 * warp;   // a then b: free now
+    const int quad = warp & 3, chalf = warp >> 2;  // TMEM lanes 32·quad.., column half
+    const int mrow0 = m0 + 32 * quad;
     const int m = mrow0 + lane;                        // phase-1 row of this thread
     const bool mok = m < ep.M;
     float rowsum = 0.f;
     float scale = 0.f;
     if constexpr (EPI == EPI_UPD || EPI == EPI_BWD) scale = update_scale(ep, z);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = chalf * CSPAN; c < (chalf + 1) * CSPAN; c += 32) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c, v);
+        tmem_ld32(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)c, v);
         const int nb = n0 + c;
         // ---- phase 1: lane = row
         if constexpr (EPI == EPI_FWD) {
@@ -321,7 +328,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         __syncwarp();
     }
     if constexpr (EPI == EPI_BWD) {
-        if (mok) ep.bias_upd[(long long)z * ep.zs_bias + m] -= scale * rowsum;   // b -= η·(Σδ/B)
+        if (mok && chalf == 0) ep.bias_upd[(long long)z * ep.zs_bias + m] -= scale * rowsum;   // b -= η·(Σδ/B)
     }
     fence_before();
     __syncthreads();
