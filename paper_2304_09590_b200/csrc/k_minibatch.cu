@@ -153,6 +153,7 @@ const char* mb_plan(const NetDesc& d, int batch) {
     if (d.n[1] % 128 != 0 || d.n[2] % 256 != 0 || d.n[1] > 4096 || d.n[2] > 4096)
         return "hidden widths must be multiples of 128 (H1) and 256 (H2)";
     if (d.n[3] > 16) return "at most 16 outputs";
+    if ((size_t)d.n[3] * d.n[2] * 2 > 48 * 1024) return "W3 (outputs × H2, bf16) must fit 48 KB of shared memory";
     return nullptr;
 }
 
@@ -289,7 +290,14 @@ __global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, Mb
 // 0 for rows past the slice (short last batch, R14).
 __global__ void __launch_bounds__(256) mb_out_fwd(const float* __restrict__ children, const int32_t* __restrict__ Y,
                                                   MbState s, long long n_local, int K_local, int z0, int step) {
+    extern __shared__ __align__(16) __nv_bfloat16 w3s[];   // [O][H2]: W3b staged once per CTA
     const int z = z0 + blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(s.W3b + (long long)z * 16 * s.H2);
+        uint4* dst = reinterpret_cast<uint4*>(w3s);
+        for (int i = threadIdx.x; i < s.O * s.H2 / 8; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
     const int b = blockIdx.x * 8 + warp;
     long long st;
     const long long cnt = slice_rows(n_local, K_local, z, &st);
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(256) mb_out_fwd(const float* __restrict__ chil
     bsz = bsz < 0 ? 0 : (bsz > s.B ? s.B : bsz);
     const float* b3 = children + (long long)z * s.P + s.woff3 + (long long)s.O * s.H2;
     const __nv_bfloat16* a2 = s.A2 + ((long long)z * s.B + b) * s.H2;
-    const __nv_bfloat16* w3 = s.W3b + (long long)z * 16 * s.H2;
+    const __nv_bfloat16* w3 = w3s;
     float acc[16];
 #pragma unroll
     for (int o = 0; o < 16; ++o) acc[o] = 0.f;
@@ -478,8 +486,8 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         f2.out_bm = s->A2; f2.out_mb = nullptr; f2.zs_act = (long long)s->H2 * B;
         if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW2b, s->tA1, s_count, s->H2, B, s->H1, f2, st))) return e;
         // output layer (CUDA cores: N = 10 / K = 10 are not dense contractions)
-        mb_out_fwd<<<dim3((unsigned)(B / 8), (unsigned)s_count), 256, 0, st>>>(children, y, *s, n_local, K_local,
-                                                                                 s_first, (int)j);
+        mb_out_fwd<<<dim3((unsigned)(B / 8), (unsigned)s_count), 256, sizeof(__nv_bfloat16) * (size_t)s->O * s->H2,
+                     st>>>(children, y, *s, n_local, K_local, s_first, (int)j);
         mb_out_bwd<<<dim3((unsigned)(s->H2 / 64), (unsigned)s_count), 256, 0, st>>>(
             children, *s, n_local, K_local, s_first, (int)j, lr);
         if ((e = cudaEventRecord(s->ev_ob, st))) return e;
