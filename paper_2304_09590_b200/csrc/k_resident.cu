@@ -74,12 +74,6 @@ constexpr int CMAX = 4;       // cluster size
 #endif
 // every warp runs F then U (instead of warps 4..7 running U before F)
 constexpr bool kV8SameOrder = PNN_V8_SAME_ORDER != 0;
-#ifndef PNN_CHAIN_V9
-#define PNN_CHAIN_V9 0
-#endif
-// v9 chain: the pair publishes h to shared memory and one warp forms the CTA's partial
-// logits lane-per-output (one row per CTA instead of a transpose-reduce row per warp)
-constexpr bool kV9 = PNN_CHAIN_V9 != 0;
 #ifndef PNN_SWEEP_XWAIT
 #define PNN_SWEEP_XWAIT 1
 #endif
@@ -99,8 +93,7 @@ struct __align__(16) Smem {
     float asum[AR][UMAX][4];           // [s % AR][row][part] partial row sums of acc(s)
     float gbuf[GR][UMAX];              // [c % GR][row] g(c)
     float zbuf[ZS][2 * CMAX][16];      // [c % ZS][2·cta + half][o] partial logits
-    float w2s[UMAX][16];               // W2[o][k0 + u] (o < 10), the CTA's units (v8 layout)
-    float w2t[16][UMAX + 4];           // the same, output-major (v9 layout; padded rows)
+    float w2s[UMAX][16];               // W2[o][k0 + u] (o < 10), the CTA's units
     float b1s[UMAX];                   // b1 of the CTA's units
     float b2s[2][16];                  // b2 before sample c at [c & 1] (identical in every CTA)
     float hs[2][UMAX];                 // h(c) of the CTA's units, [c & 1]
@@ -248,7 +241,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
         for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NW);
         for (int i = 0; i < GR; ++i) mbar_init(&sm.gready[i], 2);
-        for (int i = 0; i < ZS; ++i) mbar_init(&sm.zfull[i], kV9 ? 1 : 2);
+        for (int i = 0; i < ZS; ++i) mbar_init(&sm.zfull[i], 2);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < (S + 1) * DP; i += blockDim.x) xring[i] = 0.f;   // + zero row
@@ -256,9 +249,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 
     for (int i = threadIdx.x; i < UMAX * 16; i += blockDim.x) {
         const int u = i >> 4, o = i & 15;
-        const float wv0 = (u < Uown && o < O) ? W2[(long long)o * H + k0 + u] : 0.f;
-        sm.w2s[u][o] = wv0;
-        sm.w2t[o][u] = wv0;
+        sm.w2s[u][o] = (u < Uown && o < O) ? W2[(long long)o * H + k0 + u] : 0.f;
     }
     for (int i = threadIdx.x; i < UMAX; i += blockDim.x) sm.b1s[i] = (i < Uown) ? b1g[k0 + i] : 0.f;
     for (int i = threadIdx.x; i < 32; i += blockDim.x) (&sm.b2s[0][0])[i] = (i < O) ? b2g[i] : 0.f;
@@ -316,7 +307,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     const int half = warp & 1;
     const int uc = 32 * half + lane;               // this lane's unit in the chain
     const bool lc = uc < Uown;
-    const int zrow = kV9 ? crank : 2 * crank + half;   // this warp's / CTA's row of zbuf in every CTA
+    const int zrow = 2 * crank + half;             // this warp's row of zbuf in every CTA
     uint32_t rz[C > 1 ? C - 1 : 1];                // DSMEM address of zbuf[0][zrow][0] in each peer
     if constexpr (C > 1) {
 #pragma unroll
@@ -553,39 +544,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             // W2[o][uc] (pre-update: R6), kept for δ1 below
             float wv[12];
             const int zs = c % ZS;
-            if constexpr (kV9) {
-#pragma unroll
-                for (int o = 0; o < 12; ++o) wv[o] = (o < O) ? sm.w2t[o][uc] : 0.f;
-                sm.hs[c & 1][uc] = h;
-                named_bar_sync(1 + (warp >> 1), 64);      // the pair's h(c) is in shared memory (ids 1..4)
-                TR(8);
-                if (half == 0) {
-                    // ---- the CTA's partial logits, lane o: Σ_u W2[o][u] h_u over the 64 units ----
-                    const int o = lane < O ? lane : 0;
-                    const float4* wr = reinterpret_cast<const float4*>(&sm.w2t[o][0]);
-                    const float4* hr = reinterpret_cast<const float4*>(&sm.hs[c & 1][0]);
-                    float a[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-                    for (int q = 0; q < UMAX / 4; ++q) {
-                        const float4 w4 = wr[q], h4 = hr[q];
-                        a[q & 3] = fmaf(w4.w, h4.w, fmaf(w4.z, h4.z, fmaf(w4.y, h4.y, fmaf(w4.x, h4.x, a[q & 3]))));
-                    }
-                    const float zl = (a[0] + a[1]) + (a[2] + a[3]);
-                    const bool pub = lane < O;
-                    if (pub) sm.zbuf[zs][zrow][lane] = zl;
-                    if constexpr (C > 1) {
-#pragma unroll
-                        for (int p = 0; p < C - 1; ++p)
-                            st_async_f32_if(pub, rz[p] + zs * kZStride + lane * 4, zl,
-                                            rz[p] + kZfullOff - (uint32_t)(zrow * 64) + zs * 8);
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        if constexpr (C > 1) mbar_arrive_expect_tx(&sm.zfull[zs], (uint32_t)((C - 1) * O * 4));
-                        else mbar_arrive(&sm.zfull[zs]);
-                    }
-                }
-            } else {
             {
                 const float4* wq = reinterpret_cast<const float4*>(&sm.w2s[uc][0]);
 #pragma unroll
@@ -631,7 +589,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                     else mbar_arrive(&sm.zfull[zs]);
                 }
             }
-            }
             TR(9);
             // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
             //      which comes after their wait on gready(c) (first warp of the pair) ----
@@ -662,7 +619,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 #pragma unroll
                 for (int o = 0; o < 12; ++o) zp[o] = 0.f;
 #pragma unroll
-                for (int i = 0; i < (kV9 ? C : 2 * C); ++i) {
+                for (int i = 0; i < 2 * C; ++i) {
                     const float4* zq = reinterpret_cast<const float4*>(&sm.zbuf[zs][i][0]);
 #pragma unroll
                     for (int q = 0; q < 3; ++q) {
@@ -704,15 +661,10 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 sm.b1s[uc] -= gu;
 #pragma unroll
                 for (int o = 0; o < O; ++o) wv[o] = fmaf(-(lr * dl[o]), h, wv[o]);
-                if constexpr (kV9) {
-#pragma unroll
-                    for (int o = 0; o < O; ++o) sm.w2t[o][uc] = wv[o];
-                } else {
-                    float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
-                    wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
-                    wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
-                    wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
-                }
+                float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
+                wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+                wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
+                wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
             }
             if (half == kB2Half && lane == 0) {        // b2(c+1) into the other buffer: the pair's
                 const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);   // partner may
@@ -759,7 +711,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     float* W2o = opaque(W2);
     for (int i = threadIdx.x; i < Uown * O; i += blockDim.x) {
         const int u = i / O, o = i % O;
-        W2o[(long long)o * H + k0 + u] = kV9 ? sm.w2t[o][u] : sm.w2s[u][o];
+        W2o[(long long)o * H + k0 + u] = sm.w2s[u][o];
     }
     for (int i = threadIdx.x; i < Uown; i += blockDim.x) opaque(b1g)[k0 + i] = sm.b1s[i];
     if (crank == 0 && threadIdx.x < O) opaque(b2g)[threadIdx.x] = sm.b2s[T & 1][threadIdx.x];
@@ -878,9 +830,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
         constexpr uint32_t kAStride = 2 * UMAX * 4 * 4;
 
         auto sweep_f = [&](int s, int sx) {
-#ifndef PNN_EXP_SW_NOXWAIT
             mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));
-#endif
             const float* xn = xring + sx * DP + 4 * lane;
             uint64_t acc[R];
 #pragma unroll
@@ -900,14 +850,12 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 xa = ya; xb = yb;
                 ya = na; yb = nb;
             }
-            float px = 0.f;
-#ifndef PNN_EXP_SW_NOWX
+            float px;
             {
                 const float4 w4 = *reinterpret_cast<const float4*>(wxp);
                 const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
                 px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
             }
-#endif
             float v[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -915,9 +863,6 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 upk(acc[r], lo, hi);
                 v[r] = lo + hi;
             }
-#ifdef PNN_EXP_SW_NORED
-            const float part = v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7] + px;
-#else
             const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
             float u4[4];
 #pragma unroll
@@ -928,7 +873,6 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             for (int i = 0; i < 2; ++i)
                 u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
             const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
-#endif
             const int a = s % AR;
             st_async_f32_if(xlive, apart + (uint32_t)a * kAStride, part, abar + (uint32_t)a * 8u);
         };
@@ -940,9 +884,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
 #ifdef PNN_SPLIT_PROFILE
             const long long t0 = ptx::clock64();
 #endif
-#ifndef PNN_EXP_SW_NOGWAIT
             mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
-#endif
 #ifdef PNN_SPLIT_PROFILE
             pw_g += ptx::clock64() - t0;
 #endif
@@ -966,14 +908,12 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 xa = ya; xb = yb;
                 ya = na; yb = nb;
             }
-#ifndef PNN_EXP_SW_NOWX
             float4 w4 = *reinterpret_cast<const float4*>(wxp);
             const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
             const float gq = -sm.gbuf[u % GR][kr0 + tr];
             w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
             w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
             *reinterpret_cast<float4*>(wxp) = w4;
-#endif
         };
 
         int sx = 0;                                // ring slot of x(s)
