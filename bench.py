@@ -305,7 +305,7 @@ def main():
             tflops_tc = achieved
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                     "traffic": None,
-                    "kernel": "training epoch (bf16 mini-batch: weight cast + 8 launches per step, CUDA graph)",
+                    "kernel": "training epoch (bf16 mini-batch: weight cast + 7 launches per step, CUDA graph)",
                     "peak_note": "MEASURED_PEAKS.json hbm_gbs; algorithmic bytes per step = K_local x "
                                  "(8(W1+W2) + 4(W1+2 W2)); tensor-side: "
                                  f"{tflops_tc:.1f} TFLOP/s = {tflops_tc / pk.get('bf16_tflops_sustained', 1392.3):.3f} "
@@ -337,7 +337,7 @@ def main():
                     "flop_per_launch": flop_launch}
         import math
         steps_epoch = math.ceil(math.ceil(nrows / K_local) / cfg.batch)
-        if kernel_id == 3:          # bf16 tcgen05 mini-batch: weight cast + 8 per step
+        if kernel_id == 3:          # bf16 tcgen05 mini-batch: weight cast + 7 per step
             launches_epoch = 1 + launches_per_epoch * steps_epoch
         elif kernel_id == 4:        # fp32 mini-batch step kernels: 4 per step
             launches_epoch = launches_per_epoch * steps_epoch

@@ -95,9 +95,10 @@ extern "C" int pnn_debug_tc_gemm(const void* A, const void* B, float* C, int Z, 
 // are averaged before one update; short last batch averaged over its size, R14):
 //   cast     Xs = bf16(x rows of the batch) and its transpose XsT (rows past the slice: 0)
 //   F1 (tc)  A1 = bf16(relu(W1b·Xsᵀ + b1))            -> A1 [z][B][H1], A1T [z][H1][B]
-//   F2 (tc)  A2 = bf16(relu(W2b·A1ᵀ + b2))            -> A2 [z][B][H2]
-//   out_fwd  z3 = A2·W3bᵀ + b3, softmax, δ3 = p - e (0 past the batch), δ3b; b3 update
-//   out_bwd  dW3 = δ3bᵀ·A2 -> W3, W3b; dA2 = δ3b·W3b(old); δ2 = dA2 ⊙ [A2 > 0] -> δ2b,
+//   F2 (tc)  A2 = bf16(relu(W2b·A1ᵀ + b2))            -> A2 [z][B][H2]; its epilogue also
+//            forms each row tile's share of z3 = A2·W3bᵀ (the 10-wide output layer, fused)
+//   out_bwd  z3 = Σ tiles + b3, softmax, δ3 = p - e (0 past the batch), δ3b, b3 update;
+//            dW3 = δ3bᵀ·A2 -> W3, W3b; dA2 = δ3b·W3b(old); δ2 = dA2 ⊙ [A2 > 0] -> δ2b,
 //            δ2bT; b2 update
 //   B4 (tc)  dA1ᵀ = W2bT·δ2bᵀ (pre-update W2, R6); δ1 = dA1 ⊙ [A1T > 0] -> δ1T; b1 update
 //   B3 (tc)  dW2 = δ2bT·A1Tᵀ -> W2 -= η/B·dW2, W2b, W2bT (the other copy); runs on a side
@@ -108,10 +109,10 @@ extern "C" int pnn_debug_tc_gemm(const void* A, const void* B, float* C, int Z, 
 struct MbState {
     int K_local, D, H1, H2, O, B;
     long long P, woff1, woff2, woff3;
-    __nv_bfloat16 *W1b, *W2b, *W2bT, *W3b, *Xs, *XsT, *A1, *A1T, *A2, *d2b, *d2bT, *d1T, *d3b;
+    __nv_bfloat16 *W1b, *W2b, *W2bT, *W3b, *Xs, *XsT, *A1, *A1T, *A2, *d2b, *d2bT, *d1T;
     __nv_bfloat16* W2bT2;     // second W2ᵀ copy: step j's B4 reads [j & 1] while B3 writes the other
     __nv_bfloat16 *Xs2, *XsT2;  // second input copy: step j+1's cast runs beside step j's tail
-    float* d3;
+    float* z3part;            // [Z][H2/128][64][16]: F2's fused partial output pre-activations
     CUtensorMap tW1b, tXs, tW2b, tA1, tW2bT, td2b, td2bT, tA1T, td1T, tXsT, tW2bT2, tXs2, tXsT2;
     cudaStream_t cxs = nullptr;           // the next step's input cast (forked inside the graph)
     cudaEvent_t ev_go = nullptr, ev_cx = nullptr;
@@ -160,9 +161,9 @@ const char* mb_plan(const NetDesc& d, int batch) {
 void mb_destroy(MbState* s) {
     if (!s) return;
     __nv_bfloat16* bufs[] = {s->Xs2, s->XsT2, s->W2bT2, s->W1b, s->W2b, s->W2bT, s->W3b, s->Xs, s->XsT, s->A1, s->A1T, s->A2, s->d2b,
-                             s->d2bT, s->d1T, s->d3b};
+                             s->d2bT, s->d1T};
     for (auto* b : bufs) cudaFree(b);
-    cudaFree(s->d3);
+    cudaFree(s->z3part);
     for (auto& e : s->g)
         if (e.exec) cudaGraphExecDestroy(e.exec);
     if (s->cap) cudaStreamDestroy(s->cap);
@@ -184,12 +185,11 @@ MbState* mb_create(const NetDesc& d, int K_local, int batch, cudaError_t* err) {
     struct { __nv_bfloat16** p; long long n; } al[] = {
         {&s->W1b, Z * H1 * D}, {&s->W2b, Z * H2 * H1}, {&s->W2bT, Z * H1 * H2}, {&s->W2bT2, Z * H1 * H2}, {&s->W3b, Z * 16 * H2},
         {&s->Xs, Z * B * D}, {&s->XsT, Z * D * B}, {&s->Xs2, Z * B * D}, {&s->XsT2, Z * D * B}, {&s->A1, Z * B * H1}, {&s->A1T, Z * H1 * B},
-        {&s->A2, Z * B * H2}, {&s->d2b, Z * B * H2}, {&s->d2bT, Z * H2 * B}, {&s->d1T, Z * H1 * B},
-        {&s->d3b, Z * B * 16}};
+        {&s->A2, Z * B * H2}, {&s->d2b, Z * B * H2}, {&s->d2bT, Z * H2 * B}, {&s->d1T, Z * H1 * B}};
     *err = cudaSuccess;
     for (auto& a : al)
         if (*err == cudaSuccess) *err = cudaMalloc(a.p, sizeof(__nv_bfloat16) * (size_t)a.n);
-    if (*err == cudaSuccess) *err = cudaMalloc(&s->d3, sizeof(float) * (size_t)(Z * B * 16));
+    if (*err == cudaSuccess) *err = cudaMalloc(&s->z3part, sizeof(float) * (size_t)(Z * (H2 / tc::BM) * 64 * 16));
     if (*err == cudaSuccess) *err = cudaMemset(s->W3b, 0, sizeof(__nv_bfloat16) * (size_t)(Z * 16 * H2));
     if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
     if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
@@ -285,79 +285,14 @@ __global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, Mb
     }
 }
 
-// Output layer forward + δ3: one warp per batch row (grid: B/8 × CNs, 8 warps); z3 = A2·W3bᵀ
-// + b3 with the bf16 operands in fp32, softmax (max-subtracted, R4), δ3 = p − e (Eq.10),
-// 0 for rows past the slice (short last batch, R14).
-__global__ void __launch_bounds__(256) mb_out_fwd(const float* __restrict__ children, const int32_t* __restrict__ Y,
-                                                  MbState s, long long n_local, int K_local, int z0, int step) {
-    extern __shared__ __align__(16) __nv_bfloat16 w3s[];   // [O][H2]: W3b staged once per CTA
-    const int z = z0 + blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(s.W3b + (long long)z * 16 * s.H2);
-        uint4* dst = reinterpret_cast<uint4*>(w3s);
-        for (int i = threadIdx.x; i < s.O * s.H2 / 8; i += blockDim.x) dst[i] = src[i];
-    }
-    __syncthreads();
-    const int b = blockIdx.x * 8 + warp;
-    long long st;
-    const long long cnt = slice_rows(n_local, K_local, z, &st);
-    long long bsz = cnt - (long long)step * s.B;
-    bsz = bsz < 0 ? 0 : (bsz > s.B ? s.B : bsz);
-    const float* b3 = children + (long long)z * s.P + s.woff3 + (long long)s.O * s.H2;
-    const __nv_bfloat16* a2 = s.A2 + ((long long)z * s.B + b) * s.H2;
-    const __nv_bfloat16* w3 = w3s;
-    float acc[16];
-#pragma unroll
-    for (int o = 0; o < 16; ++o) acc[o] = 0.f;
-    for (int j = 8 * lane; j < s.H2; j += 256) {
-        const uint4 av = *reinterpret_cast<const uint4*>(a2 + j);
-        const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&av);
-        float a[8];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) { const float2 f = __bfloat1622float2(ap[q]); a[2 * q] = f.x; a[2 * q + 1] = f.y; }
-#pragma unroll
-        for (int o = 0; o < 16; ++o) {
-            if (o < s.O) {
-                const uint4 wv = *reinterpret_cast<const uint4*>(w3 + (long long)o * s.H2 + j);
-                const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&wv);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 f = __bfloat1622float2(wp[q]);
-                    acc[o] = fmaf(a[2 * q], f.x, acc[o]);
-                    acc[o] = fmaf(a[2 * q + 1], f.y, acc[o]);
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 0; o < 16; ++o)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], off);
-    float mx = -INFINITY;
-#pragma unroll
-    for (int o = 0; o < 16; ++o)
-        if (o < s.O) { acc[o] += b3[o]; mx = fmaxf(mx, acc[o]); }
-    float sum = 0.f;
-#pragma unroll
-    for (int o = 0; o < 16; ++o)
-        if (o < s.O) { acc[o] = expf(acc[o] - mx); sum += acc[o]; }
-    const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;
-#pragma unroll
-    for (int o = 0; o < 16; ++o) {
-        if (lane == o) {
-            const float dl = (o < s.O && b < bsz) ? acc[o] / sum - ((o == label) ? 1.f : 0.f) : 0.f;
-            s.d3[((long long)z * s.B + b) * 16 + o] = dl;
-            s.d3b[((long long)z * s.B + b) * 16 + o] = __float2bfloat16_rn(dl);
-        }
-    }
-}
-
 // Output layer backward (grid: H2/64 × CNs, 256 threads = 64 hidden units × 4 batch
 // quarters): dW3 = δ3bᵀ·A2 → W3, W3b; dA2 = δ3b·W3b (pre-update W3, R6); δ2 = dA2 ⊙
 // [A2 > 0] (R9) → δ2b [B][H2] and δ2bT [H2][B]; b2 -= η·Σδ2/B; block 0 also b3 -= η·Σδ3/B.
-__global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, MbState s, long long n_local,
-                                                  int K_local, int z0, int step, float lr) {
-    __shared__ float d3s[64][16];
+__global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, const int32_t* __restrict__ Y,
+                                                  MbState s, long long n_local, int K_local, int z0, int step,
+                                                  float lr) {
+    __shared__ float d3s[64][16];                  // δ3b (bf16-rounded) of the batch
+    __shared__ float d3f[64][16];                  // δ3 in fp32 (the b3 update)
     __shared__ float part[3][64][17];
     const int z = z0 + blockIdx.y;
     long long st;
@@ -365,13 +300,48 @@ __global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, 
     long long bsz = cnt - (long long)step * s.B;
     bsz = bsz < 0 ? 0 : (bsz > s.B ? s.B : bsz);
     const float scale = bsz > 0 ? lr / (float)bsz : 0.f;
-    for (int i = threadIdx.x; i < s.B * 16; i += blockDim.x)
-        (&d3s[0][0])[i] = __bfloat162float(s.d3b[(long long)z * s.B * 16 + i]);
-    __syncthreads();
     float* P = children + (long long)z * s.P;
+    // ---- output layer forward from F2's fused partials: z3 = Σ_tiles + b3, softmax (R4),
+    //      δ3 = p − e (Eq.10; 0 past the batch); every CTA of the CN computes all rows ----
+    if (threadIdx.x < 64) {
+        const int b = threadIdx.x;
+        const float* b3 = P + s.woff3 + (long long)s.O * s.H2;
+        const int nt = s.H2 / tc::BM;
+        float zz[16];
+#pragma unroll
+        for (int o = 0; o < 16; ++o) zz[o] = 0.f;
+        for (int t = 0; t < nt; ++t) {
+            const float4* zq = reinterpret_cast<const float4*>(s.z3part + (((long long)z * nt + t) * 64 + b) * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 f = zq[q];
+                zz[4 * q] += f.x; zz[4 * q + 1] += f.y; zz[4 * q + 2] += f.z; zz[4 * q + 3] += f.w;
+            }
+        }
+        const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;
+        float m = -INFINITY;
+#pragma unroll
+        for (int o = 0; o < 16; ++o)
+            if (o < s.O) { zz[o] = b3[o] + zz[o]; m = fmaxf(m, zz[o]); }
+        float sum = 0.f;
+#pragma unroll
+        for (int o = 0; o < 16; ++o)
+            if (o < s.O) { zz[o] = expf(zz[o] - m); sum += zz[o]; }
+#pragma unroll
+        for (int o = 0; o < 16; ++o) {
+            float dl = 0.f;
+            if (o < s.O && b < bsz) {
+                const float x2 = zz[o] / sum;
+                dl = x2 - ((o == label) ? 1.f : 0.f);
+            }
+            d3f[b][o] = dl;
+            d3s[b][o] = __bfloat162float(__float2bfloat16_rn(dl));
+        }
+    }
+    __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x < s.O) {        // b3 -= η·(Σ_b δ3 / B), δ3 in fp32
         float t = 0.f;
-        for (int b = 0; b < s.B; ++b) t += s.d3[((long long)z * s.B + b) * 16 + threadIdx.x];
+        for (int b = 0; b < s.B; ++b) t += d3f[b][threadIdx.x];
         P[s.woff3 + (long long)s.O * s.H2 + threadIdx.x] -= scale * t;
     }
     const int jl = threadIdx.x & 63, g = threadIdx.x >> 6;
@@ -484,12 +454,11 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         f2.M = s->H2; f2.N = B; f2.nvalid = B;
         f2.bias = children + s->woff2 + (long long)s->H2 * s->H1; f2.zs_bias = s->P;
         f2.out_bm = s->A2; f2.out_mb = nullptr; f2.zs_act = (long long)s->H2 * B;
+        f2.w3 = s->W3b; f2.z3part = s->z3part;          // the output layer's partials, fused
         if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW2b, s->tA1, s_count, s->H2, B, s->H1, f2, st))) return e;
         // output layer (CUDA cores: N = 10 / K = 10 are not dense contractions)
-        mb_out_fwd<<<dim3((unsigned)(B / 8), (unsigned)s_count), 256, sizeof(__nv_bfloat16) * (size_t)s->O * s->H2,
-                     st>>>(children, y, *s, n_local, K_local, s_first, (int)j);
         mb_out_bwd<<<dim3((unsigned)(s->H2 / 64), (unsigned)s_count), 256, 0, st>>>(
-            children, *s, n_local, K_local, s_first, (int)j, lr);
+            children, y, *s, n_local, K_local, s_first, (int)j, lr);
         if ((e = cudaEventRecord(s->ev_ob, st))) return e;
         const bool odd = (j & 1) != 0;
         // B4: δ1 = (W2bᵀ·δ2b) ⊙ [A1 > 0]; b1 update (pre-update W2: before B3)
@@ -520,7 +489,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
     return cudaGetLastError();
 }
 
-// One epoch = 1 + 8·steps launches; captured once into a CUDA graph (keyed by every
+// One epoch = 1 + 7·steps launches; captured once into a CUDA graph (keyed by every
 // argument the launches bake in) and replayed, so the host issues one launch per epoch.
 // Keep the CNs' fp32 master slabs L2-resident across the epoch's steps (every step reads and
 // writes all of them; with the bf16 copies the working set is ~106 MB for C5 < 126 MB of L2):

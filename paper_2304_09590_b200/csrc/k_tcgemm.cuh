@@ -45,6 +45,11 @@ struct Epi {
     __nv_bfloat16* out_bm;
     __nv_bfloat16* out_mb;
     long long zs_act;         // M·N elements per z for both activation layouts
+    //          optional (w3 != nullptr): the next layer's partial pre-activations of this
+    //          row tile, z3part[z][blockIdx.x][n][o] = Σ_{m in tile} w3[z][o][m]·y[m][n], o < 16
+    //          (the 10-wide output layer fused into the producing GEMM, a10)
+    const __nv_bfloat16* w3;
+    float* z3part;
     // EPI_BWD: d = acc ⊙ [mask[z][m][n] > 0]; out_mb[z][m][n] = bf16(d);
     //          bias[m] -= scale · Σ_{n < nvalid} d  (the layer's bias update)
     const __nv_bfloat16* mask;
@@ -180,7 +185,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     constexpr int STAGES = GemmSmem<BN>::STAGES;
     constexpr int NWE = threads_for(BN) / 32;     // epilogue warps: 4, or 8 (two per lane quadrant)
     constexpr int CSPAN = BN / (NWE / 4);          // columns per epilogue warp
-    static_assert(sizeof(GemmSmem<BN>::a) + sizeof(GemmSmem<BN>::b) >= NWE * 32 * 33 * sizeof(float),
+    static_assert(sizeof(GemmSmem<BN>::a) + sizeof(GemmSmem<BN>::b) >=
+                      NWE * 32 * 33 * sizeof(float) + (EPI == EPI_FWD ? 4 * BN * 16 * sizeof(float) : 0),
                   "epilogue tiles");
 
     if (threadIdx.x == 0) {
@@ -196,6 +202,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     __syncthreads();
     fence_after();
     const uint32_t tmem = s.tmem;
+    // the next layer's weights of this row tile (EPI_FWD with w3): staged while the MMAs run
+    __shared__ float w3s[EPI == EPI_FWD ? 16 * BM : 1];
+    if constexpr (EPI == EPI_FWD) {
+        if (ep.w3) {
+            for (int i = threadIdx.x; i < 16 * BM; i += blockDim.x) {
+                const int o = i / BM, r = i % BM;
+                w3s[i] = (m0 + r < ep.M) ? __bfloat162float(ep.w3[((long long)z * 16 + o) * ep.M + m0 + r]) : 0.f;
+            }
+        }
+    }
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
@@ -274,6 +290,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 for (int r = 0; r < 32; ++r)
                     if (mrow0 + r < ep.M && nok) omb[(long long)(mrow0 + r) * ep.N] = __float2bfloat16_rn(tile[r][lane]);
             }
+            if (ep.w3) {                           // this warp's 32 rows' share of z3[n][o]
+                float zp[16];
+#pragma unroll
+                for (int o = 0; o < 16; ++o) zp[o] = 0.f;
+#pragma unroll 4
+                for (int r = 0; r < 32; ++r) {
+                    const float y = tile[r][lane];
+                    const float* wr = w3s + (32 * quad + r);
+#pragma unroll
+                    for (int o = 0; o < 16; ++o) zp[o] = fmaf(wr[o * BM], y, zp[o]);
+                }
+                float* zr = reinterpret_cast<float*>(&s.a[0][0]) + NWE * 32 * 33;   // [4][BN][16]
+#pragma unroll
+                for (int o = 0; o < 16; ++o) zr[(quad * BN + (c + lane)) * 16 + o] = zp[o];
+            }
         } else if constexpr (EPI == EPI_BWD) {
             // d = acc ⊙ [mask > 0] (ReLU'(z) from the stored activation, R9), mask [m][n]
             const __nv_bfloat16* mk = ep.mask + (long long)z * ep.zs_act + n;
@@ -326,6 +357,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         }
         __syncwarp();
+    }
+    if constexpr (EPI == EPI_FWD) {
+        if (ep.w3) {                               // sum the 4 row groups, in order
+            __syncthreads();
+            const float* zr = reinterpret_cast<const float*>(&s.a[0][0]) + NWE * 32 * 33;
+            for (int i = threadIdx.x; i < BN * 16; i += blockDim.x) {
+                const float t = ((zr[i] + zr[BN * 16 + i]) + zr[2 * BN * 16 + i]) + zr[3 * BN * 16 + i];
+                if (n0 + i / 16 < ep.nvalid)
+                    ep.z3part[(((long long)z * gridDim.x + blockIdx.x) * ep.N + n0 + i / 16) * 16 + (i % 16)] = t;
+            }
+        }
     }
     if constexpr (EPI == EPI_BWD) {
         if (mok && chalf == 0) ep.bias_upd[(long long)z * ep.zs_bias + m] -= scale * rowsum;   // b -= η·(Σδ/B)

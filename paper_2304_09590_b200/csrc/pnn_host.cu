@@ -574,8 +574,8 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     ResidentPlan plan{};
     int k = choose_kernel(net, &plan);
     *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
-    // resident: Gram terms + training; tc bf16: weight cast + 8 per mini-batch step
-    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 8 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
+    // resident: Gram terms + training; tc bf16: weight cast + 7 per mini-batch step
+    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
     return PNN_OK;
 }
 
