@@ -3,7 +3,7 @@ ReLU/ReLU/softmax, batch 64) against the oracle's bf16 mode (reading R25: the
 same rounding points), through the C ABI.  Marked gpu.
 
 Bar (BASELINE.json north_star "bf16 mini-batch within 2e-2 relative"; DESIGN.md
-§3 R25): per tensor (every W^l, b^l of every CN and of the merged net)
+§3 R31): per layer (W^l and b^l together, of every CN and of the merged net)
 ‖P_gpu − P_oracle‖_F / ‖P_oracle‖_F ≤ 2e-2.  That bar is loose against the
 size of one epoch's update, so the test also bounds the difference by a
 fraction of the update itself, ‖P_gpu − P_oracle‖_F ≤ 0.1·‖P_oracle − P_0‖_F:
@@ -40,16 +40,29 @@ def _tensors(layers, P):
     return out
 
 
+def _layers(layers, P):
+    out, o = [], 0
+    for l in range(1, len(layers)):
+        n = layers[l] * layers[l - 1] + layers[l]
+        out.append((f"layer {l}", P[..., o:o + n]))
+        o += n
+    return out
+
+
 def _check(layers, got, ref, p0, what):
+    # the north_star bar, per layer (W^l and b^l together; reading R31)
+    for (name, g), (_, r) in zip(_layers(layers, got), _layers(layers, ref)):
+        rel = np.linalg.norm(g.astype(np.float64) - r) / max(np.linalg.norm(r.astype(np.float64)), 1e-30)
+        assert rel <= 2e-2, f"{what} {name}: relative Frobenius {rel:.3e} > 2e-2"
+    # the bug detector, per tensor: the difference is a small fraction of the epoch's update
     for (name, g), (_, r), (_, z) in zip(_tensors(layers, got), _tensors(layers, ref), _tensors(layers, p0)):
         d = np.linalg.norm((g.astype(np.float64) - r))
-        rel = d / max(np.linalg.norm(r.astype(np.float64)), 1e-30)
         upd = np.linalg.norm(r.astype(np.float64) - z)
-        assert rel <= 2e-2, f"{what} {name}: relative Frobenius {rel:.3e} > 2e-2"
         assert d <= 0.1 * upd + 1e-7, f"{what} {name}: |gpu-oracle| {d:.3e} vs update {upd:.3e}"
 
 
-@pytest.mark.parametrize("K,n,epochs", [(3, 3 * 150 + 2, 2), (2, 2 * 64, 1)])
+@pytest.mark.parametrize("K,n,epochs", [(3, 3 * 150 + 2, 2), (2, 2 * 64, 1),
+                                        (8, 8 * 145 + 5, 1)])   # C5's K = 8: the bench's launch grid
 def test_c5_reduced_matches_oracle_bf16(orc, K, n, epochs):
     from paper_2304_09590_b200 import PNN
     from paper_2304_09590_b200.pnn import PNN_BF16, PNN_KERNEL_TC_BF16
@@ -66,7 +79,7 @@ def test_c5_reduced_matches_oracle_bf16(orc, K, n, epochs):
     kids = np.stack([net.get_params(i) for i in range(K)])
     merged = net.get_params(-1)
     okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=epochs, batch=64,
-                                   threads=K, precision="bf16")
+                                   threads=min(K, 8), precision="bf16")
     p0 = orc.init_params(c.layers, c.init, 0)
     for i in range(K):
         _check(c.layers, kids[i], okids[i], p0, f"CN {i}")
