@@ -287,10 +287,25 @@ def test_error_paths():
     with pytest.raises(PnnError) as e:
         net.train_epoch(dev(np.tile(X, (4, 1))), dev(np.tile(y, 4)))   # 20 rows: slice 2 < batch 4
     assert e.value.status == 3
+    with pytest.raises(PnnError) as e:
+        net.set_slots(-1)
+    assert e.value.status == 1
+    Xt, yt = make_split(16, "test", 0)
+    with pytest.raises(PnnError) as e:
+        net.evaluate(dev(Xt[:0]), dev(yt[:0]))              # n = 0
+    assert e.value.status == 1
+    with pytest.raises(PnnError) as e:
+        net.evaluate(dev(Xt), dev(yt), subnet=8)            # not a local CN
+    assert e.value.status == 1
+    with pytest.raises(PnnError) as e:
+        net.set_kernel(3)                                   # PNN_KERNEL_TC_BF16: not settable
+    assert e.value.status == 1
     # the handle is still usable after validation errors
     X, y = make_split(64, "train", 0)
     net.train_epoch(dev(X), dev(y))
     torch.cuda.synchronize()
+    acc, conf, cost = net.evaluate(dev(Xt), dev(yt), subnet=0)
+    assert 0.0 <= acc <= 1.0 and 0.1 <= conf <= 1.0 and cost >= 0.0
 
 
 def test_set_params_roundtrip_and_predict_subnet(orc):
