@@ -313,11 +313,14 @@ def main():
                     "bytes_per_step": bytes_step, "train_ms_per_launch": train_ms, "flop_per_launch": flop_launch}
         else:
             traffic = None
+            ncu_extra = None
             try:      # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch,
                       # from the committed ncu --set full capture of this workload
                 tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(cfg.name)
                 if tr and K_local == cfg.K and kernel_id == 2:
                     traffic = tr["bytes_per_launch"]
+                    ncu_extra = {k: tr[k] for k in ("fma_pipe_active_pct", "issue_active_pct", "smem_tbs",
+                                                    "smem_peak_tbs", "smem_frac", "note", "source") if k in tr}
             except Exception:  # noqa: BLE001
                 traffic = None
             roof = {"bound": "alu", "achieved": achieved, "peak": peak_max,
@@ -335,6 +338,8 @@ def main():
                                  f"is {achieved / (peak_max * sm_mhz / pk.get('sm_max_mhz', 1965.0)):.3f}",
                     "train_ms_per_launch": train_ms,
                     "flop_per_launch": flop_launch}
+            if ncu_extra:
+                roof["ncu"] = ncu_extra
         import math
         steps_epoch = math.ceil(math.ceil(nrows / K_local) / cfg.batch)
         if kernel_id == 3:          # bf16 tcgen05 mini-batch: weight cast + 7 per step
