@@ -643,11 +643,15 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                     for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
                     TR(10);
                 } else {
+                    // element-wise output (sigmoid / tanh, ½-SSE: Eq.9, R11): lane o forms output
+                    // o's activation and δ2 once, then every lane takes the ten by shuffles
+                    float zsel = z2[0];
 #pragma unroll
-                    for (int o = 0; o < O; ++o) {
-                        const float x2 = act_fwd_t<A2>(z2[o]);
-                        dl[o] = (x2 - ((o == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
-                    }
+                    for (int o = 1; o < O; ++o) zsel = (lane == o) ? z2[o] : zsel;
+                    const float x2 = act_fwd_t<A2>(zsel);
+                    const float dmine = (x2 - ((lane == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = __shfl_sync(0xffffffffu, dmine, o);
                 }
             }
             // ---- δ1, g(c) of unit uc; W2(c+1), b1(c+1), b2(c+1) ----
@@ -1056,11 +1060,15 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
 #pragma unroll
                     for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
                 } else {
+                    // element-wise output (sigmoid / tanh, ½-SSE: Eq.9, R11): lane o forms output
+                    // o's activation and δ2 once, then every lane takes the ten by shuffles
+                    float zsel = z2[0];
 #pragma unroll
-                    for (int o = 0; o < O; ++o) {
-                        const float x2 = act_fwd_t<A2>(z2[o]);
-                        dl[o] = (x2 - ((o == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
-                    }
+                    for (int o = 1; o < O; ++o) zsel = (lane == o) ? z2[o] : zsel;
+                    const float x2 = act_fwd_t<A2>(zsel);
+                    const float dmine = (x2 - ((lane == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = __shfl_sync(0xffffffffu, dmine, o);
                 }
             }
             // ---- δ1, g(c) → the owning sweep CTA; W2, b1, b2 updates (registers) ----
