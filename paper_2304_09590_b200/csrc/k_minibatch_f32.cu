@@ -161,35 +161,30 @@ __global__ void __launch_bounds__(256) f32_out(const float* __restrict__ childre
     }
 #pragma unroll
     for (int o = 0; o < OMAX; ++o) acc[o] = warp_sum(acc[o]);
-    float x[OMAX];
+    // lane o < O forms output o (one exp per lane instead of O per lane)
+    float zmine = acc[0] + b2[0];
+#pragma unroll
+    for (int o = 1; o < OMAX; ++o)
+        if (o < O && lane == o) zmine = acc[o] + b2[o];
+    float xmine;
     if constexpr (A2 == PNN_SOFTMAX) {
-        float m = -INFINITY;
+        float m = -INFINITY;                       // max-subtracted (R4)
 #pragma unroll
         for (int o = 0; o < OMAX; ++o)
-            if (o < O) { acc[o] += b2[o]; m = fmaxf(m, acc[o]); }
-        float s = 0.f;
-#pragma unroll
-        for (int o = 0; o < OMAX; ++o)
-            if (o < O) { x[o] = expf(acc[o] - m); s += x[o]; }
-#pragma unroll
-        for (int o = 0; o < OMAX; ++o)
-            if (o < O) x[o] = x[o] / s;
+            if (o < O) m = fmaxf(m, acc[o] + b2[o]);
+        const float e = (lane < O) ? expf(zmine - m) : 0.f;
+        xmine = e / warp_sum(e);
     } else {
-#pragma unroll
-        for (int o = 0; o < OMAX; ++o)
-            if (o < O) x[o] = act_fwd_t<A2>(acc[o] + b2[o]);
+        xmine = act_fwd_t<A2>(zmine);
     }
     const int label = (b < bsz) ? Y[row0 + b] : -1;
-#pragma unroll
-    for (int o = 0; o < OMAX; ++o) {
-        if (o < O && lane == o) {
-            float dl = 0.f;
-            if (b < bsz) {
-                const float e = (o == label) ? 1.f : 0.f;
-                dl = (A2 == PNN_SOFTMAX) ? x[o] - e : (x[o] - e) * act_deriv_t<A2>(x[o]);
-            }
-            D2buf[((long long)z * BMAX + b) * OMAX + o] = dl;
+    if (lane < O) {
+        float dl = 0.f;
+        if (b < bsz) {
+            const float e = (lane == label) ? 1.f : 0.f;
+            dl = (A2 == PNN_SOFTMAX) ? xmine - e : (xmine - e) * act_deriv_t<A2>(xmine);
         }
+        D2buf[((long long)z * BMAX + b) * OMAX + lane] = dl;
     }
 }
 
