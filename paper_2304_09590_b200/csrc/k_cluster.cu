@@ -37,7 +37,8 @@ constexpr int kAhead = 2;         // rows in flight
 
 struct ClusterPlanDev {
     int C;                                   // cluster size
-    int rows[PNN_MAX_LAYERS + 1];            // ⌈n_l / C⌉ rows per CTA per layer
+    int rows[PNN_MAX_LAYERS + 1];            // ⌈n_l / C⌉ rows per CTA per layer (n_l if replicated)
+    int rep[PNN_MAX_LAYERS + 1];             // layer held in full by every CTA (the small output layer)
     int w_off[PNN_MAX_LAYERS + 1];           // own W^l rows in shared memory (floats)
     int b_off[PNN_MAX_LAYERS + 1];           // own b^l
     int x_off[PNN_MAX_LAYERS + 1];           // full x^l, parity 0 (parity 1 at + x_par)
@@ -159,7 +160,7 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
 
     // ---- own rows of every layer into shared memory ----
     for (int l = 1; l <= L; ++l) {
-        const int nin = d.n[l - 1], nout = d.n[l], R = pl.rows[l], k0 = r * R;
+        const int nin = d.n[l - 1], nout = d.n[l], R = pl.rows[l], k0 = pl.rep[l] ? 0 : r * R;
         const float* Wg = P + d.woff[l];
         const float* bg = Wg + (long long)nout * nin;
         for (int i = tid; i < R * nin; i += kThreads) {
@@ -192,7 +193,7 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
     // per-layer tables in shared memory: indexing kernel parameters by a runtime layer
     // number compiles to slow indexed constant loads on the per-sample path
     __shared__ struct {
-        int n[PNN_MAX_LAYERS + 1], act[PNN_MAX_LAYERS + 1], rows[PNN_MAX_LAYERS + 1];
+        int n[PNN_MAX_LAYERS + 1], act[PNN_MAX_LAYERS + 1], rows[PNN_MAX_LAYERS + 1], rep[PNN_MAX_LAYERS + 1];
         int w_off[PNN_MAX_LAYERS + 1], b_off[PNN_MAX_LAYERS + 1], x_off[PNN_MAX_LAYERS + 1],
             d_off[PNN_MAX_LAYERS + 1];
     } sp;
@@ -200,6 +201,7 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         sp.n[tid] = d.n[tid];
         sp.act[tid] = tid < PNN_MAX_LAYERS ? d.act[tid] : 0;
         sp.rows[tid] = pl.rows[tid];
+        sp.rep[tid] = pl.rep[tid];
         sp.w_off[tid] = pl.w_off[tid];
         sp.b_off[tid] = pl.b_off[tid];
         sp.x_off[tid] = pl.x_off[tid];
@@ -226,12 +228,13 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         const float* x0 = smf + pl.ring_off + slot * pl.ring_stride;
         // ---------------- forward ----------------
         for (int l = 1; l <= L; ++l) {
-            const int nin = sp.n[l - 1], nout = sp.n[l], R = sp.rows[l], k0 = r * R;
+            const bool rep = sp.rep[l] != 0;
+            const int nin = sp.n[l - 1], nout = sp.n[l], R = sp.rows[l], k0 = rep ? 0 : r * R;
             const float* xin = (l == 1) ? x0 : smf + sp.x_off[l - 1] + par * pl.x_par;
             const int xo = sp.x_off[l] + par * pl.x_par;
             const int a = sp.act[l - 1];
             const int own = max(0, min(R, nout - k0));
-            if (tid == 0) mbar_arrive_expect_tx(&fbar[l][par], 4u * (uint32_t)(nout - own));
+            if (tid == 0 && !rep) mbar_arrive_expect_tx(&fbar[l][par], 4u * (uint32_t)(nout - own));
             const uint32_t fb = smem_u32(&fbar[l][par]);
             XRegs xr;
             xr.load(xin, nin, lane);
@@ -242,14 +245,16 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
                 const float acc = warp_sum(xr.ok ? xr.dot(w, nin, lane) : dot_lanes(w, xin, nin, lane));
                 const float z = acc + smf[sp.b_off[l] + i];
                 const float v = (a == PNN_SOFTMAX) ? z : act_fwd(a, z);
-                if (lane == r) smf[xo + k] = v;
+                if (rep) {                         // replicated layer: every CTA computes every row
+                    if (lane == 0) smf[xo + k] = v;
+                } else if (lane == r) smf[xo + k] = v;
                 else if (lane < C)                 // into peer `lane`'s x^l, completing its fbar
                     st_async_f32(mapa(sbase + 4u * (uint32_t)(xo + k), (uint32_t)lane), v, mapa(fb, (uint32_t)lane));
             }
             PROF(2);
             __syncthreads();                       // own rows of x^l written
             PROF(3);
-            mbar_wait(&fbar[l][par], (uint32_t)((t >> 1) & 1));   // peers' rows landed
+            if (!rep) mbar_wait(&fbar[l][par], (uint32_t)((t >> 1) & 1));   // peers' rows landed
             PROF(4);
             if (a == PNN_SOFTMAX) {                // the output layer's softmax, redundantly per CTA
                 if (warp == 0) softmax_warp(smf + xo, nout, lane);
@@ -258,7 +263,7 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         }
         // ---------------- δ^L, own rows ----------------
         {
-            const int nL = sp.n[L], R = sp.rows[L], k0 = r * R, aL = sp.act[L - 1];
+            const int nL = sp.n[L], R = sp.rows[L], k0 = sp.rep[L] ? 0 : r * R, aL = sp.act[L - 1];
             const float* xL = smf + sp.x_off[L] + par * pl.x_par;
             for (int i = tid; i < R; i += kThreads) {
                 const int k = k0 + i;
@@ -274,6 +279,22 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         // ---------------- δ^l, l = L-1..1: reduce-scatter of the partials ----------------
         for (int l = L - 1; l >= 1; --l) {
             const int nl = sp.n[l], Rn = sp.rows[l + 1], Rl = sp.rows[l];
+            if (sp.rep[l + 1]) {
+                // W^{l+1} and δ^{l+1} are complete in every CTA: δ^l of the own units directly
+                const float* Wn = smf + sp.w_off[l + 1];      // pre-update (R6)
+                const float* dn = smf + sp.d_off[l + 1];
+                const float* xl = smf + sp.x_off[l] + par * pl.x_par;
+                const int k0 = r * Rl;
+                for (int i = tid; i < Rl; i += kThreads) {
+                    const int k = k0 + i;
+                    float acc = 0.f;
+                    if (k < nl)
+                        for (int q = 0; q < Rn; ++q) acc = fmaf(Wn[q * nl + k], dn[q], acc);
+                    smf[sp.d_off[l] + i] = (k < nl) ? acc * act_deriv_from_x(sp.act[l - 1], xl[k]) : 0.f;
+                }
+                __syncthreads();
+                continue;
+            }
             const float* Wn = smf + sp.w_off[l + 1];          // own rows of W^{l+1}, pre-update (R6)
             const float* dn = smf + sp.d_off[l + 1];
             const int rv = pl.recv_off + par * pl.recv_par + l * pl.recv_layer;   // per layer: no reuse
@@ -306,7 +327,7 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
         }
         // ---------------- update (Eqs.12-13), own rows ----------------
         for (int l = 1; l <= L; ++l) {
-            const int nin = sp.n[l - 1], nout = sp.n[l], R = sp.rows[l], k0 = r * R;
+            const int nin = sp.n[l - 1], nout = sp.n[l], R = sp.rows[l], k0 = sp.rep[l] ? 0 : r * R;
             const float* xin = (l == 1) ? x0 : smf + sp.x_off[l - 1] + par * pl.x_par;
             XRegs xr;
             xr.load(xin, nin, lane);
@@ -333,7 +354,8 @@ sgd_cluster_kernel(NetDesc d, ClusterPlanDev pl, float* __restrict__ children, c
 #undef PROF
     // ---- write back own rows ----
     for (int l = 1; l <= L; ++l) {
-        const int nin = d.n[l - 1], nout = d.n[l], R = pl.rows[l], k0 = r * R;
+        if (pl.rep[l] && r != 0) continue;          // replicated layer: identical copies, CTA 0 writes
+        const int nin = d.n[l - 1], nout = d.n[l], R = pl.rows[l], k0 = pl.rep[l] ? 0 : r * R;
         float* Wg = P + d.woff[l];
         float* bg = Wg + (long long)nout * nin;
         for (int i = tid; i < R * nin; i += kThreads) {
@@ -352,7 +374,10 @@ bool make_plan(const NetDesc& d, int C, ClusterPlanDev* pl) {
     int off = 0;
     int rmax = 1;
     for (int l = 1; l <= d.L; ++l) {
-        p.rows[l] = (d.n[l] + C - 1) / C;
+        // the output layer, when small, is replicated in every CTA and updated redundantly: its
+        // forward needs no all-gather and the next δ no reduce-scatter (two exchanges fewer)
+        p.rep[l] = (C > 1 && l == d.L && (long long)d.n[l] * d.n[l - 1] <= 4096) ? 1 : 0;
+        p.rows[l] = p.rep[l] ? d.n[l] : (d.n[l] + C - 1) / C;
         rmax = p.rows[l] > rmax ? p.rows[l] : rmax;
         p.w_off[l] = off;
         off += p.rows[l] * d.n[l - 1];
