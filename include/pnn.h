@@ -226,6 +226,14 @@ pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count);
  * Errors: PNN_ERR_INVALID.                                                  */
 pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches_per_epoch);
 
+/* Measurement hook: enable = 1 starts recording a pair of CUDA events around every
+ * training-kernel launch that follows (on the caller's stream; the resident path
+ * brackets its SGD kernel, not the Gram pre-pass; the mini-batch paths their epoch
+ * graph); enable = 0 stops, waits for the recorded events and returns the mean
+ * launch duration in ms and the number of launches (either pointer may be NULL).
+ * Errors: PNN_ERR_INVALID (NULL handle), PNN_ERR_CUDA.                           */
+pnn_status pnn_kernel_timing(pnn_net net, int32_t enable, double* mean_ms, int32_t* count);
+
 /* Last error message of this handle (or of the last failed pnn_create when
  * net is NULL).  Never NULL; valid until the next call on the handle.        */
 const char* pnn_last_error(pnn_net net);

@@ -1228,13 +1228,30 @@ ResidentPlan plan_resident(const NetDesc& d, int batch) {
     return p;
 }
 
+static cudaError_t launch_sgd_resident_only(const ResidentPlan& p, const NetDesc& d, float* children,
+                                            const float* x, const float4* rec, long long n_local, int K_local,
+                                            int s_first, int s_count, float lr, cudaStream_t st);
+
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
                                 const float* x, const int32_t* labels, float4* rec, long long n_local,
-                                int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
+                                int K_local, int s_first, int s_count, float lr, cudaStream_t st,
+                                cudaEvent_t ev0, cudaEvent_t ev1) {
     if (s_count <= 0) return cudaSuccess;
     gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (ev0) {                                     // timing hook: bracket the SGD launch only
+        if ((e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
+        e = launch_sgd_resident_only(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+        if (e != cudaSuccess) return e;
+        return cudaEventRecord(ev1, st);
+    }
+    return launch_sgd_resident_only(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
+}
+
+static cudaError_t launch_sgd_resident_only(const ResidentPlan& p, const NetDesc& d, float* children,
+                                            const float* x, const float4* rec, long long n_local, int K_local,
+                                            int s_first, int s_count, float lr, cudaStream_t st) {
     if (p.variant == 10) {
         if (p.cluster == 2) return launch_split<1>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
         if (p.cluster == 3) return launch_split<2>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);

@@ -27,6 +27,8 @@ struct pnn_net_s {
     void* comm = nullptr;             // ncclComm_t
     int batch = 1, precision = PNN_FP32, kernel = PNN_KERNEL_AUTO;
     int slots = 0;                    // CNs trained concurrently (0 = all local CNs; f4)
+    bool timing = false;              // record CUDA events around each training-kernel launch
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
     float* d_children = nullptr;      // [K_local][P]
     float* d_merged = nullptr;        // [P]
     double* d_msum = nullptr;         // [P] fp64 partial sums (multi-rank merge)
@@ -193,6 +195,13 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
     int k = choose_kernel(net, &plan);
     if (k < 0) return fail(net, PNN_ERR_INVALID, "forced kernel not valid here: %s", plan.why);
     cudaError_t e;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (net->timing && s_count > 0) {
+        CUDA_TRY(net, cudaEventCreate(&ev0));
+        CUDA_TRY(net, cudaEventCreate(&ev1));
+        net->tev.emplace_back(ev0, ev1);
+        if (k != PNN_KERNEL_RESIDENT) CUDA_TRY(net, cudaEventRecord(ev0, st));   // the resident path
+    }                                                                               // brackets its SGD launch
     if (k == PNN_KERNEL_TC_BF16) {
         if (!net->mb) {
             net->mb = mb_create(net->d, net->K_local, net->batch, &e);
@@ -223,7 +232,7 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
             net->gram_rows = n;
         }
         e = launch_sgd_resident(plan, net->d, net->d_children, x, y, net->d_gram, n, net->K_local,
-                                s_first, s_count, net->lr, st);
+                                s_first, s_count, net->lr, st, ev0, ev1);
     } else {
         if (net->batch > 1 && !net->d_gscratch)
             CUDA_TRY(net, cudaMalloc(&net->d_gscratch,
@@ -232,6 +241,7 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
                                  net->lr, net->batch, net->d_gscratch, st);
     }
     if (e != cudaSuccess) return fail(net, PNN_ERR_CUDA, "training launch: %s", cudaGetErrorString(e));
+    if (ev1 && k != PNN_KERNEL_RESIDENT) CUDA_TRY(net, cudaEventRecord(ev1, st));
     return PNN_OK;
 }
 
@@ -385,6 +395,28 @@ pnn_status pnn_set_slots(pnn_net net, int32_t slots) {
     if (st) return st;
     if (slots < 0) return fail(net, PNN_ERR_INVALID, "slots = %d < 0", slots);
     net->slots = slots;
+    return PNN_OK;
+}
+
+pnn_status pnn_kernel_timing(pnn_net net, int32_t enable, double* mean_ms, int32_t* count) {
+    if (!net) return PNN_ERR_INVALID;
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    double total = 0.0;
+    int32_t cnt = 0;
+    for (auto& pr : net->tev) {
+        float ms = 0.f;
+        if (!enable && cudaEventSynchronize(pr.second) == cudaSuccess &&
+            cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) {
+            total += ms;
+            ++cnt;
+        }
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    net->tev.clear();
+    net->timing = enable != 0;
+    if (mean_ms) *mean_ms = cnt ? total / cnt : 0.0;
+    if (count) *count = cnt;
     return PNN_OK;
 }
 
@@ -594,6 +626,7 @@ pnn_status pnn_destroy(pnn_net net) {
     cudaFree(net->d_gscratch);
     mb_destroy(net->mb);
     mb32_destroy(net->mb32);
+    for (auto& pr : net->tev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     cudaFree(net->d_eval);
     cudaFree(net->d_gram);
     cudaFree(net->d_xstage);

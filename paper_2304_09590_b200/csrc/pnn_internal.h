@@ -56,7 +56,7 @@ ResidentPlan plan_resident(const NetDesc& d, int batch);
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
                                 const float* x, const int32_t* labels, float4* gram, long long n_local,
                                 int K_local, int s_first, int s_count, float lr,
-                                cudaStream_t st);
+                                cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // Cluster kernel (k_cluster.cu): any depth, weights resident in the shared memory of a
 // cluster of C <= 8 CTAs, per-sample SGD.

@@ -34,7 +34,7 @@ KERNEL = {"auto": PNN_KERNEL_AUTO, "reference": PNN_KERNEL_REFERENCE, "resident"
 EXPORTS = ["pnn_create", "pnn_set_comm", "pnn_set_minibatch", "pnn_set_kernel", "pnn_train_epoch",
            "pnn_train_epoch_host", "pnn_merge", "pnn_predict", "pnn_get_params", "pnn_set_params",
            "pnn_device_params", "pnn_param_count", "pnn_local_subnets", "pnn_kernel_info",
-           "pnn_last_error", "pnn_destroy", "pnn_evaluate", "pnn_set_slots"]
+           "pnn_last_error", "pnn_destroy", "pnn_evaluate", "pnn_set_slots", "pnn_kernel_timing"]
 
 _lib = None
 
@@ -77,6 +77,7 @@ def load(path: str | None = None):
         "pnn_destroy": ([V], I32),
         "pnn_evaluate": ([V, I32, V, V, I64, V, V], I32),
         "pnn_set_slots": ([V, I32], I32),
+        "pnn_kernel_timing": ([V, I32, V, V], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -189,6 +190,13 @@ class PNN:
                                          x.shape[0], out.ctypes.data_as(ctypes.c_void_p),
                                          ctypes.c_void_p(_stream_ptr(stream))))
         return tuple(float(v) for v in out)
+
+    def kernel_timing(self, enable):
+        """Start (True) / stop (False) recording CUDA events around the training-kernel
+        launches; stopping returns (mean ms per launch, launches)."""
+        ms, n = ctypes.c_double(), ctypes.c_int32()
+        self._check(self._L.pnn_kernel_timing(self.h, 1 if enable else 0, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def set_slots(self, slots):
         self._check(self._L.pnn_set_slots(self.h, int(slots)))
