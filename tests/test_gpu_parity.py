@@ -212,6 +212,20 @@ def test_resident_v10_split_variant(orc, monkeypatch):
         assert np.abs(merged - omerged).max() < TOL, name
 
 
+def test_kernel_timing_hook():
+    """pnn_kernel_timing brackets each training-kernel launch with CUDA events."""
+    c = CONFIGS["C4"]
+    X, y = make_split(16 * 40, "train", 0)
+    net = PNN(c.layers, c.act, c.init, 16, c.lr, seed=0)
+    net.kernel_timing(True)
+    for _ in range(3):
+        net.train_epoch(dev(X), dev(y))
+    ms, n = net.kernel_timing(False)
+    assert n == 3 and ms > 0.0
+    net.train_epoch(dev(X), dev(y))          # stopped: nothing recorded
+    assert net.kernel_timing(False) == (0.0, 0)
+
+
 def test_determinism_and_kernel_agreement(orc):
     c = CONFIGS["C4"]
     X, y = make_split(32 * 64, "train", 0)
