@@ -1,4 +1,5 @@
-"""Tiny runs of every training path (resident, cluster, reference, fp32 and bf16 mini-batch) with\nmerge, predict and evaluate — a quick all-kernels check (tools only; compute-sanitizer is closed\non this pool)."""
+"""Tiny runs of every training path (resident, cluster, reference, fp32 and bf16 mini-batch) with
+merge, predict and evaluate: a quick all-kernels check (tools only)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
