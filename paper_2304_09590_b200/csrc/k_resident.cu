@@ -1188,6 +1188,14 @@ cudaError_t launch_c(const ResidentPlan& p, const NetDesc& d, float* children, c
 
 }  // namespace
 
+// The Gram-record pre-pass, for other kernels that use the same lookahead (k_deep.cu).
+cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
+                        int s_count, float4* rec, cudaStream_t st) {
+    if (s_count <= 0) return cudaSuccess;
+    gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, D, n_local, K_local, s_first, s_count, rec);
+    return cudaGetLastError();
+}
+
 ResidentPlan plan_resident(const NetDesc& d, int batch) {
     ResidentPlan p{};
     auto no = [&](const char* why) {

@@ -202,6 +202,14 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         net->tev.emplace_back(ev0, ev1);
         if (k != PNN_KERNEL_RESIDENT) CUDA_TRY(net, cudaEventRecord(ev0, st));   // the resident path
     }                                                                               // brackets its SGD launch
+    const bool deep = k == PNN_KERNEL_CLUSTER && !deep_plan(net->d, net->batch);
+    if ((k == PNN_KERNEL_RESIDENT || deep) && net->gram_rows < n) {   // 32-B Gram records (R27)
+        cudaFree(net->d_gram);
+        net->d_gram = nullptr;
+        net->gram_rows = 0;
+        CUDA_TRY(net, cudaMalloc(&net->d_gram, 2 * sizeof(float4) * (size_t)n));
+        net->gram_rows = n;
+    }
     if (k == PNN_KERNEL_TC_BF16) {
         if (!net->mb) {
             net->mb = mb_create(net->d, net->K_local, net->batch, &e);
@@ -220,17 +228,13 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         }
         e = launch_minibatch_f32(net->mb32, net->d, net->d_children, x, y, n, net->K_local, s_first, s_count,
                                  net->lr, st);
+    } else if (deep) {                                       // 3-layer shapes: W¹ in registers
+        e = launch_sgd_deep(net->d, net->d_children, x, y, net->d_gram, n, net->K_local, s_first, s_count,
+                            net->lr, st);
     } else if (k == PNN_KERNEL_CLUSTER) {
-        const ClusterPlan cp = plan_cluster(net->d, net->batch);
-        e = launch_sgd_cluster(cp, net->d, net->d_children, x, y, n, net->K_local, s_first, s_count, net->lr, st);
+        e = launch_sgd_cluster(plan_cluster(net->d, net->batch), net->d, net->d_children, x, y, n, net->K_local,
+                               s_first, s_count, net->lr, st);
     } else if (k == PNN_KERNEL_RESIDENT) {
-        if (net->gram_rows < n) {
-            cudaFree(net->d_gram);
-            net->d_gram = nullptr;
-            net->gram_rows = 0;
-            CUDA_TRY(net, cudaMalloc(&net->d_gram, 2 * sizeof(float4) * (size_t)n));   // 32-B records
-            net->gram_rows = n;
-        }
         e = launch_sgd_resident(plan, net->d, net->d_children, x, y, net->d_gram, n, net->K_local,
                                 s_first, s_count, net->lr, st, ev0, ev1);
     } else {
@@ -455,7 +459,9 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         const int k = choose_kernel(net, &rp);
         int cap = net->K_local;                   // CNs that run concurrently
         if (k == PNN_KERNEL_RESIDENT) cap = 148 / (rp.cluster > 0 ? rp.cluster : 1);
-        else if (k == PNN_KERNEL_CLUSTER) cap = 148 / plan_cluster(net->d, net->batch).cluster;
+        else if (k == PNN_KERNEL_CLUSTER)
+            cap = 148 / (deep_plan(net->d, net->batch) ? plan_cluster(net->d, net->batch).cluster
+                                                       : deep_cluster_size(net->d));
         else if (k == PNN_KERNEL_REFERENCE) cap = 148;
         groups = net->K_local / (cap > 0 ? cap : 1);
         groups = groups < 1 ? 1 : (groups > 8 ? 8 : groups);
@@ -607,7 +613,9 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     int k = choose_kernel(net, &plan);
     *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
     // resident: Gram terms + training; tc bf16: weight cast + 7 per mini-batch step
-    *launches = (k == PNN_KERNEL_RESIDENT) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
+    // deep cluster variant (3 layers): Gram terms + training
+    const bool deep = k == PNN_KERNEL_CLUSTER && !deep_plan(net->d, net->batch);
+    *launches = (k == PNN_KERNEL_RESIDENT || deep) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
     return PNN_OK;
 }
 

@@ -58,6 +58,18 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 int K_local, int s_first, int s_count, float lr,
                                 cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
+// The lookahead's Gram records (32 B per row: x(u-4..u-1)·x(u) and the label), k_resident.cu.
+cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
+                        int s_count, float4* rec, cudaStream_t st);
+
+// Deep kernel (k_deep.cu): 3-layer nets D-H1-H2-O, W¹ rows register-resident across a cluster of
+// 8 CTAs with the R27 lookahead, layers 2-3 and the per-sample chain on dedicated warps.
+const char* deep_plan(const NetDesc& d, int batch);   // nullptr when supported
+int deep_cluster_size(const NetDesc& d);
+cudaError_t launch_sgd_deep(const NetDesc& d, float* children, const float* x, const int32_t* labels,
+                            float4* rec, long long n_local, int K_local, int s_first, int s_count, float lr,
+                            cudaStream_t st);
+
 // Cluster kernel (k_cluster.cu): any depth, weights resident in the shared memory of a
 // cluster of C <= 8 CTAs, per-sample SGD.
 struct ClusterPlan {

@@ -1,0 +1,91 @@
+"""GPU parity of the deep cluster variant (k_deep.cu: 3-layer nets, W¹ rows in the
+registers of a cluster of 4 or 8 CTAs, R27 lookahead) against the fp32 oracle.
+
+The variant is what the cluster kernel (and AUTO) runs for 3-layer shapes with
+768 < D <= 784, H1 <= 320, O <= 16 and per-sample SGD (C3: 784-300-100-10);
+PNN_DEEP=0 falls back to the generic cluster kernel.  Tolerance as everywhere for
+fp32 per-sample SGD: max-abs 1e-4 on every parameter (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+import torch
+
+from datagen import make_split
+from workloads import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _run(orc, layers, act, init, K, lr, n, epochs=1, kernel="auto", deep=True):
+    from paper_2304_09590_b200 import PNN
+    X, y = make_split(n, "train", 0)
+    X = np.ascontiguousarray(X[:, :layers[0]])
+    net = PNN(layers, act, init, K, lr, seed=0)
+    net.set_kernel(kernel)
+    kinfo = net.kernel_info()
+    xd, yd = dev(X), dev(y)
+    for _ in range(epochs):
+        net.train_epoch(xd, yd)
+    net.merge()
+    torch.cuda.synchronize()
+    kids = np.stack([net.get_params(i) for i in range(K)])
+    okids, omerged = orc.train_pnn(layers, act, init, K, lr, 0, X, y, epochs=epochs, threads=8)
+    err = np.abs(kids - okids).max(axis=1)
+    assert err.max() < TOL, f"per-CN max-abs {err}"
+    assert np.abs(net.get_params(-1) - omerged).max() < TOL
+    return kinfo
+
+
+def test_c3_shape_auto(orc):
+    """C3 (784-300-100-10 tanh/tanh/softmax, Xavier, η=0.01), 8 CNs, ragged slices,
+    2 epochs: AUTO picks the cluster kernel's deep variant (2 launches per epoch)."""
+    c = CONFIGS["C3"]
+    kinfo = _run(orc, c.layers, c.act, c.init, 8, c.lr, 8 * 150 + 5, epochs=2)
+    assert tuple(kinfo) == (5, 2)
+
+
+@pytest.mark.parametrize("layers,act", [
+    ([784, 300, 100, 10], ["relu", "relu", "softmax"]),          # (lr 0.01: see below)
+    ([784, 300, 100, 10], ["sigmoid", "sigmoid", "sigmoid"]),
+    ([784, 256, 64, 10], ["leaky_relu", "leaky_relu", "softmax"]),
+    ([784, 150, 60, 10], ["tanh", "tanh", "softmax"]),          # 4-CTA clusters
+    ([784, 37, 10, 3], ["sigmoid", "sigmoid", "softmax"]),      # idle rows / warps
+    ([772, 320, 120, 16], ["tanh", "tanh", "softmax"]),         # widest; D < 784
+])
+def test_shapes_and_activations(orc, layers, act):
+    # η = 0.01 (C3's): at η = 0.05 a ReLU unit of one CN sits at z ≈ 0 where fp32
+    # summation order decides φ' ∈ {0, 1} (the R24 envelope), seen as 1.5e-4 on that CN only
+    kinfo = _run(orc, layers, act, "xavier", 5, 0.01, 5 * 90 + 3, kernel="cluster")
+    assert tuple(kinfo) == (5, 2)
+
+
+@pytest.mark.parametrize("rows_per_cn", [1, 2, 3, 5, 9, 17])
+def test_short_slices(orc, rows_per_cn):
+    """Slices shorter than the lookahead (L = 4), the prefetch depth (8) and the ring (16)."""
+    c = CONFIGS["C3"]
+    K = 6
+    n = K * rows_per_cn + (1 if rows_per_cn > 1 else 0)
+    _run(orc, c.layers, c.act, c.init, K, 0.05, n, epochs=2)
+
+
+def test_generic_cluster_fallback(orc, monkeypatch):
+    """PNN_DEEP=0: the generic cluster kernel (weights in shared memory) on the C3 shape."""
+    monkeypatch.setenv("PNN_DEEP", "0")
+    c = CONFIGS["C3"]
+    kinfo = _run(orc, c.layers, c.act, c.init, 4, c.lr, 4 * 100 + 3, kernel="cluster")
+    assert tuple(kinfo) == (5, 1)
