@@ -323,7 +323,7 @@ def main():
             try:      # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch,
                       # from the committed ncu --set full capture of this workload
                 tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(cfg.name)
-                if tr and K_local == cfg.K and kernel_id == 2:
+                if tr and K_local == cfg.K and kernel_id in (2, 5):
                     traffic = tr["bytes_per_launch"]
                     ncu_extra = {k: tr[k] for k in ("fma_pipe_active_pct", "issue_active_pct", "smem_tbs",
                                                     "smem_peak_tbs", "smem_frac", "note", "source") if k in tr}
@@ -335,7 +335,9 @@ def main():
                                     "X 4·784·rows + 32-B Gram records·rows + 2·4·P_total·K",
                     "kernel": {1: "training epoch (reference kernel)",
                                2: "persistent SGD launch (library CUDA events around it; frac_epoch adds the Gram pre-pass)",
-                               5: "training epoch (cluster kernel, weights in cluster shared memory)",
+                               5: ("training epoch (deep cluster variant: Gram pre-pass + W1 register-resident over "
+                                   "an 8-CTA cluster, k_deep.cu)" if launches_per_epoch == 2 else
+                                   "training epoch (cluster kernel, weights in cluster shared memory)"),
                                4: "training epoch (fp32 mini-batch: 4 launches per step, CUDA graph)"}
                               .get(kernel_id, "training epoch"),
                     "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
