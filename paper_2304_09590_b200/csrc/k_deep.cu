@@ -376,7 +376,8 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 mbar_arrive_expect_tx(&sm.d1full[par], 16u * (uint32_t)(g1own * NCW * C));
             }
             mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));   // every sweep's F(c)
-            mbar_wait(&sm.xfull[cs], (uint32_t)((c / S) & 1));         // (landed long ago)
+            // x(c) and its Gram record are visible through aready(c): every sweep waited xfull
+            // for x(c) before its F(c) (acquire) and arrived aready(c) after it (release)
             // every sweep has passed U(c-1): the slot of x(c-1-L) is free for x(c+PF)
             if (ct == 2 * 32 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
             const float4 G = *reinterpret_cast<const float4*>(xring + cs * DP + GOFF);
