@@ -91,7 +91,12 @@ enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          
        PNN_KERNEL_CLUSTER = 5    /* per-sample SGD, any depth, weights resident
                                     in the shared memory of a cluster of <= 8
                                     CTAs (AUTO's choice when the resident
-                                    kernel does not cover the shape, e.g. C3) */ };
+                                    kernel does not cover the shape, e.g. C3).
+                                    3-layer nets with 768 < D <= 784, H1 <= 320,
+                                    H2 <= 120, O <= 16 run its deep variant
+                                    (W1 in registers, k_deep.cu; 2 launches per
+                                    epoch in pnn_kernel_info); environment
+                                    PNN_DEEP=0 selects the generic kernel.    */ };
 
 /* Build a PNN of n_subnets CNs with layer sizes layers[0..n_layers-1]
  * (layers[0] = inputs, e.g. {784,128,10}; n_layers >= 2, each size >= 1,
