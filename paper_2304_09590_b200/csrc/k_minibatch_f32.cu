@@ -20,7 +20,7 @@
 
 struct Mb32State {
     int K_local, B;
-    float *A1 = nullptr, *D1 = nullptr, *D2 = nullptr;
+    float *A1 = nullptr, *A1P = nullptr, *D1 = nullptr, *D2 = nullptr;
     cudaStream_t cap = nullptr;
     struct G {
         cudaGraphExec_t exec = nullptr;
@@ -49,18 +49,22 @@ __device__ __forceinline__ long long batch_rows(long long n_local, int K_local, 
     return b;
 }
 
-// fwd1: a 64 (hidden) × 32 (batch) tile of Z1 per CTA, 256 threads × (4 h × 2 b), k-tiles of
-// 32 staged transposed in shared memory (W1 as [k][h], x as [k][b]) and prefetched into
-// registers one tile ahead: 8 FMA per 2 shared loads.
-constexpr int GH = 64, GB = 32, GK = 32;
-template <int A1>
+// fwd1: a 64 (hidden) × 32 (batch) tile of one K-split's partial Z1 per CTA, 256 threads ×
+// (4 h × 2 b), k-tiles of 32 staged transposed in shared memory (W1 as [k][h], x as [k][b])
+// and prefetched into registers one tile ahead: 8 FMA per 2 shared loads.  The input
+// dimension is split KS ways (grid.y = batch tile × KS) so a step fills the GPU; the
+// partials go to A1P[ks] and f32_out sums them in a fixed order.
+constexpr int GH = 64, GB = 32, GK = 32, KS = 4;
 __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ children, const float* __restrict__ X,
-                                                float* __restrict__ A1buf, NetDesc d, long long n_local,
+                                                float* __restrict__ A1P, NetDesc d, long long n_local,
                                                 int K_local, int z0, int step, int B) {
     __shared__ __align__(16) float ws[GK][GH + 4];
     __shared__ __align__(16) float xs[GK][GB + 4];
-    const int z = z0 + blockIdx.z, h0 = blockIdx.x * GH, b0 = blockIdx.y * GB;
+    const int nbt = (B + GB - 1) / GB, ks = blockIdx.y / nbt;
+    const int z = z0 + blockIdx.z, h0 = blockIdx.x * GH, b0 = (blockIdx.y - ks * nbt) * GB;
     const int D = d.n[0], H = d.n[1];
+    const int chunk = (((D + KS - 1) / KS) + GK - 1) / GK * GK;
+    const int kb = ks * chunk, ke = min(D, kb + chunk);
     long long row0;
     const long long bsz = batch_rows(n_local, K_local, z, step, B, &row0);
     const float* W1 = children + (long long)z * d.P + d.woff[1];
@@ -75,14 +79,14 @@ __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ childr
         for (int q = 0; q < 2; ++q) {
             const int slot = tid + 256 * q;                 // 0..511: row = slot >> 3, k = 4·(slot & 7)
             const int r = slot >> 3, kk = k0 + 4 * (slot & 7);
-            const bool ok = h0 + r < H && kk < D;
+            const bool ok = h0 + r < H && kk < ke;
             const float2* src = reinterpret_cast<const float2*>(W1 + (long long)(h0 + r) * D + kk);
             wr[2 * q] = ok ? src[0] : make_float2(0.f, 0.f);
             wr[2 * q + 1] = ok ? src[1] : make_float2(0.f, 0.f);
         }
         {
             const int r = tid >> 3, kk = k0 + 4 * (tid & 7);
-            const bool ok = b0 + r < bsz && kk < D;
+            const bool ok = b0 + r < bsz && kk < ke;
             xr = ok ? *reinterpret_cast<const float4*>(X + (row0 + b0 + r) * D + kk) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
@@ -97,13 +101,13 @@ __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ childr
         const int r = tid >> 3, kk = 4 * (tid & 7);
         xs[kk][r] = xr.x; xs[kk + 1][r] = xr.y; xs[kk + 2][r] = xr.z; xs[kk + 3][r] = xr.w;
     };
-    load_tile(0);
+    load_tile(kb);
     store_tile();
     __syncthreads();
-    for (int k0 = 0; k0 < D; k0 += GK) {
-        const bool more = k0 + GK < D;
+    for (int k0 = kb; k0 < ke; k0 += GK) {
+        const bool more = k0 + GK < ke;
         if (more) load_tile(k0 + GK);
-        const int kn = (D - k0) < GK ? (D - k0) : GK;
+        const int kn = (ke - k0) < GK ? (ke - k0) : GK;
 #pragma unroll 8
         for (int k = 0; k < kn; ++k) {
             const float4 w4 = *reinterpret_cast<const float4*>(&ws[k][4 * hg]);
@@ -119,24 +123,25 @@ __global__ void __launch_bounds__(256) f32_fwd1(const float* __restrict__ childr
             __syncthreads();
         }
     }
-    const float* b1 = children + (long long)z * d.P + d.woff[1] + (long long)H * D;
+    const long long zoff = ((long long)ks * K_local + z) * BMAX;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int b = b0 + 2 * bg + j;
         if (b >= B) continue;
-        float* dst = A1buf + ((long long)z * BMAX + b) * H;
+        float* dst = A1P + (zoff + b) * H;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int h = h0 + 4 * hg + i;
-            if (h < H) dst[h] = (b < bsz) ? act_fwd_t<A1>(acc[i][j] + b1[h]) : 0.f;
+            if (h < H) dst[h] = acc[i][j];
         }
     }
 }
 
-// output layer + δ2: one warp per batch row
-template <int A2>
+// a1 = φ1(Σ_ks partials + b1) (fixed order), then the output layer + δ2: one warp per batch row
+template <int A1, int A2>
 __global__ void __launch_bounds__(256) f32_out(const float* __restrict__ children, const int32_t* __restrict__ Y,
-                                               const float* __restrict__ A1buf, float* __restrict__ D2buf,
+                                               const float* __restrict__ A1P, float* __restrict__ A1buf,
+                                               float* __restrict__ D2buf,
                                                NetDesc d, long long n_local, int K_local, int z0, int step, int B) {
     extern __shared__ float w2s[];                 // [O][H]: W2 staged once per CTA
     const int z = z0 + blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,12 +154,19 @@ __global__ void __launch_bounds__(256) f32_out(const float* __restrict__ childre
     long long row0;
     const long long bsz = batch_rows(n_local, K_local, z, step, B, &row0);
     const float* b2 = W2 + (long long)O * H;
-    const float* a1 = A1buf + ((long long)z * BMAX + b) * H;
+    const float* b1 = children + (long long)z * d.P + d.woff[1] + (long long)H * d.n[0];
+    float* a1 = A1buf + ((long long)z * BMAX + b) * H;
+    const long long pstride = (long long)K_local * BMAX * H;
+    const float* p0 = A1P + ((long long)z * BMAX + b) * H;
     float acc[OMAX];
 #pragma unroll
     for (int o = 0; o < OMAX; ++o) acc[o] = 0.f;
     for (int h = lane; h < H; h += 32) {
-        const float a = a1[h];
+        float zs = p0[h];
+#pragma unroll
+        for (int q = 1; q < KS; ++q) zs += p0[q * pstride + h];
+        const float a = (b < bsz) ? act_fwd_t<A1>(zs + b1[h]) : 0.f;
+        a1[h] = a;
 #pragma unroll
         for (int o = 0; o < OMAX; ++o)
             if (o < O) acc[o] = fmaf(w2s[o * H + h], a, acc[o]);
@@ -316,10 +328,10 @@ template <int A1, int A2>
 cudaError_t enqueue_step(Mb32State* s, const NetDesc& d, float* children, const float* x, const int32_t* y,
                          long long n_local, int K_local, int z0, int zc, int step, float lr, cudaStream_t st) {
     const int H = d.n[1], D = d.n[0], B = s->B;
-    f32_fwd1<A1><<<dim3((unsigned)((H + GH - 1) / GH), (unsigned)((B + GB - 1) / GB), (unsigned)zc), 256, 0, st>>>(
-        children, x, s->A1, d, n_local, K_local, z0, step, B);
-    f32_out<A2><<<dim3((unsigned)((B + 7) / 8), (unsigned)zc), 256, sizeof(float) * (size_t)d.n[2] * H, st>>>(
-        children, y, s->A1, s->D2, d, n_local, K_local, z0, step, B);
+    f32_fwd1<<<dim3((unsigned)((H + GH - 1) / GH), (unsigned)(((B + GB - 1) / GB) * KS), (unsigned)zc), 256, 0, st>>>(
+        children, x, s->A1P, d, n_local, K_local, z0, step, B);
+    f32_out<A1, A2><<<dim3((unsigned)((B + 7) / 8), (unsigned)zc), 256, sizeof(float) * (size_t)d.n[2] * H, st>>>(
+        children, y, s->A1P, s->A1, s->D2, d, n_local, K_local, z0, step, B);
     f32_hid<A1><<<dim3((unsigned)((H + 63) / 64), (unsigned)zc), 256, 0, st>>>(children, s->A1, s->D2, s->D1, d,
                                                                                n_local, K_local, z0, step, B, lr);
     f32_upd1<<<dim3((unsigned)((H + UT - 1) / UT), (unsigned)((D + UT - 1) / UT), (unsigned)zc), 256, 0, st>>>(
@@ -374,6 +386,7 @@ const char* mb32_plan(const NetDesc& d, int batch) {
 void mb32_destroy(Mb32State* s) {
     if (!s) return;
     cudaFree(s->A1);
+    cudaFree(s->A1P);
     cudaFree(s->D1);
     cudaFree(s->D2);
     for (auto& e : s->g)
@@ -388,6 +401,7 @@ Mb32State* mb32_create(const NetDesc& d, int K_local, int batch, cudaError_t* er
     s->B = batch;
     const size_t Z = (size_t)K_local, H = (size_t)d.n[1];
     *err = cudaMalloc(&s->A1, sizeof(float) * Z * BMAX * H);
+    if (*err == cudaSuccess) *err = cudaMalloc(&s->A1P, sizeof(float) * KS * Z * BMAX * H);
     if (*err == cudaSuccess) *err = cudaMalloc(&s->D1, sizeof(float) * Z * BMAX * H);
     if (*err == cudaSuccess) *err = cudaMalloc(&s->D2, sizeof(float) * Z * BMAX * OMAX);
     if (*err == cudaSuccess) *err = cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking);
