@@ -338,7 +338,9 @@ def main():
                                5: ("training epoch (deep cluster variant: Gram pre-pass + W1 register-resident over "
                                    "an 8-CTA cluster, k_deep.cu)" if launches_per_epoch == 2 else
                                    "training epoch (cluster kernel, weights in cluster shared memory)"),
-                               4: "training epoch (fp32 mini-batch: 4 launches per step, CUDA graph)"}
+                               4: "training epoch (fp32 mini-batch: 4 launches per step, CUDA graph)",
+                               6: "training epoch (fp32 mini-batch, one persistent launch: W1 register-resident "
+                                  "over a cluster, k_mbres.cu)"}
                               .get(kernel_id, "training epoch"),
                     "peak_note": f"FP32 FMA: {sms} SMs x 128 FMA/clk x 2 flop x "
                                  f"{pk.get('sm_max_mhz', 1965.0):.0f} MHz (guide unit counts, "
@@ -368,7 +370,7 @@ def main():
                                    f"{cfg.n_train} rows, {cfg.epochs} epoch(s), batch {cfg.batch}, "
                                    f"lr {cfg.lr}",
                        "K_local": K_local, "rows_per_rank": nrows, "test_rows": cfg.n_test,
-                       "kernel": ["auto", "reference", "resident", "tc_bf16", "mb_f32", "cluster"][kernel_id],
+                       "kernel": ["auto", "reference", "resident", "tc_bf16", "mb_f32", "cluster", "mb_resident"][kernel_id],
                        "l2": f"inputs {X.nbytes / 2**20:.0f} MiB per rank > 126 MB L2 (no flush)"},
             "roofline": roof,
             "breakdown_ms": {"train": train_ms * cfg.epochs, "merge_predict": ms - train_ms * cfg.epochs},

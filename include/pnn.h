@@ -88,6 +88,13 @@ enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          
        PNN_KERNEL_MB_F32 = 4,    /* fp32 mini-batch step kernels (D-H-O nets,
                                     batch 2..64; AUTO picks it, REFERENCE
                                     opts out), reported, not settable        */
+       PNN_KERNEL_MB_RESIDENT = 6, /* fp32 mini-batch as one persistent launch per
+                                    epoch: W1 in the registers of a cluster of
+                                    ceil(H/32) CTAs (k_mbres.cu; D-H-O nets,
+                                    768 < D <= 784, H <= 256, O <= 16, batch
+                                    2..64).  AUTO's first choice for fp32
+                                    mini-batch; environment PNN_MBRES=0 falls
+                                    back to _MB_F32; reported, not settable   */
        PNN_KERNEL_CLUSTER = 5    /* per-sample SGD, any depth, weights resident
                                     in the shared memory of a cluster of <= 8
                                     CTAs (AUTO's choice when the resident
@@ -227,7 +234,8 @@ pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count);
 /* Which training kernel the next pnn_train_epoch launches (PNN_KERNEL_*),
  * and how many kernel launches it makes (PNN_KERNEL_TC_BF16: launches per
  * mini-batch step; an epoch makes 1 + that × ceil(longest slice / batch);
- * PNN_KERNEL_MB_F32: per step, an epoch makes that × ceil(longest slice / batch)).
+ * PNN_KERNEL_MB_F32: per step, an epoch makes that × ceil(longest slice / batch);
+ * PNN_KERNEL_MB_RESIDENT: per epoch).
  * Errors: PNN_ERR_INVALID.                                                  */
 pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches_per_epoch);
 

@@ -163,6 +163,8 @@ pnn_status alloc_local(pnn_net net) {
 
 int choose_kernel(pnn_net net, ResidentPlan* plan) {
     if (net->precision == PNN_BF16) return PNN_KERNEL_TC_BF16;
+    if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1 && !mbres_plan(net->d, net->batch))
+        return PNN_KERNEL_MB_RESIDENT;
     if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1 && !mb32_plan(net->d, net->batch))
         return PNN_KERNEL_MB_F32;
     if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
@@ -228,6 +230,8 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         }
         e = launch_minibatch_f32(net->mb32, net->d, net->d_children, x, y, n, net->K_local, s_first, s_count,
                                  net->lr, st);
+    } else if (k == PNN_KERNEL_MB_RESIDENT) {
+        e = launch_mbres(net->d, net->d_children, x, y, n, net->K_local, s_first, s_count, net->batch, net->lr, st);
     } else if (deep) {                                       // 3-layer shapes: W¹ in registers
         e = launch_sgd_deep(net->d, net->d_children, x, y, net->d_gram, n, net->K_local, s_first, s_count,
                             net->lr, st);
@@ -380,7 +384,7 @@ pnn_status pnn_set_kernel(pnn_net net, int32_t kernel) {
     pnn_status st = check_live(net);
     if (st) return st;
     if (kernel < PNN_KERNEL_AUTO || kernel > PNN_KERNEL_CLUSTER || kernel == PNN_KERNEL_TC_BF16 ||
-        kernel == PNN_KERNEL_MB_F32)
+        kernel == PNN_KERNEL_MB_F32)                     // (PNN_KERNEL_MB_RESIDENT = 6: reported only)
         return fail(net, PNN_ERR_INVALID, "kernel = %d unknown or not settable", kernel);
     if (kernel == PNN_KERNEL_CLUSTER) {
         ClusterPlan p = plan_cluster(net->d, net->batch);
@@ -463,6 +467,7 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
             cap = 148 / (deep_plan(net->d, net->batch) ? plan_cluster(net->d, net->batch).cluster
                                                        : deep_cluster_size(net->d));
         else if (k == PNN_KERNEL_REFERENCE) cap = 148;
+        else if (k == PNN_KERNEL_MB_RESIDENT) cap = 148 / mbres_cluster(net->d);
         groups = net->K_local / (cap > 0 ? cap : 1);
         groups = groups < 1 ? 1 : (groups > 8 ? 8 : groups);
     }
@@ -616,6 +621,7 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     // deep cluster variant (3 layers): Gram terms + training
     const bool deep = k == PNN_KERNEL_CLUSTER && !deep_plan(net->d, net->batch);
     *launches = (k == PNN_KERNEL_RESIDENT || deep) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
+    // (PNN_KERNEL_MB_RESIDENT: 1 per epoch)
     return PNN_OK;
 }
 

@@ -96,6 +96,11 @@ cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children,
 // fp32 mini-batch kernels for D-H-O nets (k_minibatch_f32.cu; f1): nullptr when supported.
 struct Mb32State;
 const char* mb32_plan(const NetDesc& d, int batch);
+// Resident fp32 mini-batch kernel (k_mbres.cu): one launch per epoch, W¹ in registers.
+const char* mbres_plan(const NetDesc& d, int batch);   // nullptr when supported
+int mbres_cluster(const NetDesc& d);
+cudaError_t launch_mbres(const NetDesc& d, float* children, const float* x, const int32_t* y, long long n_local,
+                         int K_local, int s_first, int s_count, int B, float lr, cudaStream_t st);
 Mb32State* mb32_create(const NetDesc& d, int K_local, int batch, cudaError_t* err);
 void mb32_destroy(Mb32State* s);
 cudaError_t launch_minibatch_f32(Mb32State* s, const NetDesc& d, float* children, const float* x,

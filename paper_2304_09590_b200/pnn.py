@@ -23,7 +23,7 @@ PNN_SIGMOID, PNN_TANH, PNN_RELU, PNN_SOFTMAX, PNN_LEAKY_RELU = 0, 1, 2, 3, 4
 PNN_INIT_NORMAL, PNN_INIT_UNIFORM, PNN_INIT_XAVIER_NORMAL, PNN_INIT_HE_NORMAL = 0, 1, 2, 3
 PNN_FP32, PNN_BF16 = 0, 1
 PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16, PNN_KERNEL_MB_F32, \
-    PNN_KERNEL_CLUSTER = 0, 1, 2, 3, 4, 5
+    PNN_KERNEL_CLUSTER, PNN_KERNEL_MB_RESIDENT = 0, 1, 2, 3, 4, 5, 6
 ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX,
        "leaky_relu": PNN_LEAKY_RELU}
 INIT = {"normal": PNN_INIT_NORMAL, "uniform": PNN_INIT_UNIFORM, "xavier": PNN_INIT_XAVIER_NORMAL,

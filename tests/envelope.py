@@ -59,14 +59,32 @@ def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1):
     return np.concatenate([np.concatenate([W[l].ravel().numpy(), b[l].numpy()]) for l in range(L)])
 
 
-def perturbation_envelope(orc, layers, act, params, X, y, lr, epochs=1, trials=3, seed=1):
+def perturbation_envelope(orc, layers, act, params, X, y, lr, epochs=1, trials=3, seed=1, batch=1):
     """max over `trials` of max-abs(oracle(params ± 1 ulp) - oracle(params)), fp32."""
     rng = np.random.default_rng(seed)
     p0 = np.asarray(params, np.float32)
-    ref = orc.train(layers, act, p0, X, y, lr, epochs)
+    ref = orc.train(layers, act, p0, X, y, lr, epochs, batch=batch)
     worst = 0.0
     for _ in range(trials):
         direction = np.where(rng.random(p0.size) < 0.5, np.inf, -np.inf).astype(np.float32)
         pp = np.nextafter(p0, direction).astype(np.float32)
-        worst = max(worst, float(np.abs(orc.train(layers, act, pp, X, y, lr, epochs) - ref).max()))
+        worst = max(worst, float(np.abs(orc.train(layers, act, pp, X, y, lr, epochs, batch=batch) - ref).max()))
     return worst
+
+
+def check_minibatch_cns(orc, layers, act, init, K, lr, X, y, kids, okids, epochs, batch, tol=1e-4):
+    """R22's per-CN rule for mini-batch runs: max-abs < tol, or <= 2x the oracle's own
+    1-ulp perturbation envelope on that CN's slice (N(0,1)-init ReLU nets are as
+    ill-conditioned in fp32 as C2)."""
+    p0 = orc.init_params(layers, init, 0)
+    start, count = orc.shard_bounds(len(y), K)
+    report = []
+    for i in range(K):
+        err = float(np.abs(kids[i] - okids[i]).max())
+        env = None
+        if err >= tol:
+            a, b = int(start[i]), int(start[i] + count[i])
+            env = perturbation_envelope(orc, layers, act, p0, X[a:b], y[a:b], lr, epochs, batch=batch)
+        report.append((i, err, env))
+        assert err < tol or err <= 2 * env, f"CN {i}: max-abs {err:.3g}, fp32 envelope {env}"
+    return report
