@@ -87,4 +87,5 @@ def check_minibatch_cns(orc, layers, act, init, K, lr, X, y, kids, okids, epochs
             env = perturbation_envelope(orc, layers, act, p0, X[a:b], y[a:b], lr, epochs, batch=batch)
         report.append((i, err, env))
         assert err < tol or err <= 2 * env, f"CN {i}: max-abs {err:.3g}, fp32 envelope {env}"
+    print("per-CN (index, max-abs vs oracle, fp32 envelope):", report)
     return report
