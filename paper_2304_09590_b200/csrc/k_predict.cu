@@ -42,29 +42,40 @@ predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restr
             const float* Wl = params + d.woff[l];
             const float* bl = Wl + (long long)nout * nin;
             double* out = hb[(l - 1) & 1];
-            for (int k = warp; k < nout; k += kWarps) {
-                const float* w = Wl + (long long)k * nin;
-                double acc[TILE];
+            // a warp forms KB neurons × TILE samples at once (each x value read from shared
+            // memory feeds KB fmas); the per-lane partial sums then go through a transpose-reduce
+            // whose pairing (xor 16, 8, 4, 2, 1) is that of warp_sum_d, so z is bit-identical
+            constexpr int KB = 32 / TILE;
+            const double* inp = (l == 1) ? xin : inD;
+            for (int k0 = warp * KB; k0 < nout; k0 += kWarps * KB) {
+                double acc[KB * TILE];
 #pragma unroll
-                for (int s = 0; s < TILE; ++s) acc[s] = 0.0;
-                if (l == 1) {
-                    for (int j = lane; j < nin; j += 32) {
-                        const double wj = (double)w[j];
+                for (int i = 0; i < KB * TILE; ++i) acc[i] = 0.0;
+                for (int j = lane; j < nin; j += 32) {
+                    double xv[TILE];
 #pragma unroll
-                        for (int s = 0; s < TILE; ++s) acc[s] = fma(wj, xin[s * W + j], acc[s]);
-                    }
-                } else {
-                    for (int j = lane; j < nin; j += 32) {
-                        const double wj = (double)w[j];
+                    for (int s = 0; s < TILE; ++s) xv[s] = inp[s * W + j];
 #pragma unroll
-                        for (int s = 0; s < TILE; ++s) acc[s] = fma(wj, inD[s * Hm + j], acc[s]);
+                    for (int kk = 0; kk < KB; ++kk) {
+                        const double wj = (k0 + kk < nout) ? (double)Wl[(long long)(k0 + kk) * nin + j] : 0.0;
+#pragma unroll
+                        for (int s = 0; s < TILE; ++s) acc[kk * TILE + s] = fma(wj, xv[s], acc[kk * TILE + s]);
                     }
                 }
 #pragma unroll
-                for (int s = 0; s < TILE; ++s) {
-                    double z = warp_sum_d(acc[s]) + (double)bl[k];
+                for (int h = 16; h >= 1; h >>= 1) {      // 32 values → lane l holds value l
+                    const bool up = lane & h;
+#pragma unroll
+                    for (int i = 0; i < h; ++i) {
+                        const double keep = up ? acc[i + h] : acc[i], give = up ? acc[i] : acc[i + h];
+                        acc[i] = keep + __shfl_xor_sync(0xffffffffu, give, h);
+                    }
+                }
+                const int kk = lane / TILE, s = lane % TILE, k = k0 + kk;
+                if (k < nout) {
+                    const double z = acc[0] + (double)bl[k];
                     // softmax is monotone: the readout only needs z^L (R19)
-                    if (lane == 0) out[s * Hm + k] = (l == d.L) ? z : act_fwd_d(d.act[l - 1], z);
+                    out[s * Hm + k] = (l == d.L) ? z : act_fwd_d(d.act[l - 1], z);
                 }
             }
             __syncthreads();
