@@ -1196,7 +1196,7 @@ cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long 
     return cudaGetLastError();
 }
 
-ResidentPlan plan_resident(const NetDesc& d, int batch) {
+ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent) {
     ResidentPlan p{};
     auto no = [&](const char* why) {
         p.ok = false;
@@ -1224,10 +1224,15 @@ ResidentPlan plan_resident(const NetDesc& d, int batch) {
     p.threads = NW * 32;                           // 8 warps; rows >= U are idle
     p.smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
     p.variant = 8;
-    // v10 (the chain on its own CTA) for H <= 128: 1 or 2 sweep CTAs + 1 chain CTA.  Opt-in
-    // (PNN_RESIDENT_V10=1): measured slower than v8 on C4
+    // v10 (the chain on its own CTA) for H <= 128: 1 or 2 sweep CTAs + 1 chain CTA.  It costs one
+    // SM more per CN but shortens the per-sample period: measured faster when every CN runs at
+    // once (C2 +11 %, C1 +5 %), slower when the SMs are the limit (C4: 43.6 vs 64.4 M samples/s;
+    // DESIGN.md §5).  AUTO takes it when `concurrent` CNs × its cluster fit the 148 SMs;
+    // PNN_RESIDENT_V10=1 / =0 force it on / off.
     const char* v10 = getenv("PNN_RESIDENT_V10");
-    if (H <= 2 * UMAX && v10 && v10[0] == '1') {
+    const int c10 = (H + UMAX - 1) / UMAX + 1;
+    const bool want10 = v10 && v10[0] ? v10[0] == '1' : (concurrent > 0 && (long long)concurrent * c10 <= 148);
+    if (H <= 2 * UMAX && want10) {
         p.variant = 10;
         p.cluster = (H + UMAX - 1) / UMAX + 1;
         p.smem = kSplitHead + sizeof(float) * (size_t)S * DP;

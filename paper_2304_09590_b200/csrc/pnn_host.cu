@@ -169,7 +169,8 @@ int choose_kernel(pnn_net net, ResidentPlan* plan) {
         return PNN_KERNEL_MB_F32;
     if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
     if (net->kernel == PNN_KERNEL_CLUSTER) return plan_cluster(net->d, net->batch).ok ? PNN_KERNEL_CLUSTER : -1;
-    *plan = plan_resident(net->d, net->batch);
+    const int conc = (net->slots > 0 && net->slots < net->K_local) ? net->slots : net->K_local;
+    *plan = plan_resident(net->d, net->batch, conc);
     if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
     if (plan->ok) return PNN_KERNEL_RESIDENT;
     return plan_cluster(net->d, net->batch).ok ? PNN_KERNEL_CLUSTER : PNN_KERNEL_REFERENCE;

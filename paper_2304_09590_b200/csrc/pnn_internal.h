@@ -50,7 +50,8 @@ struct ResidentPlan {
     int variant;        // template instance id
     char why[160];      // reason when !ok
 };
-ResidentPlan plan_resident(const NetDesc& d, int batch);
+// concurrent: CNs trained at once (0 = unknown: v8); see plan_resident's v10 rule
+ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent = 0);
 // gram: scratch of 2·n_local float4 (32-B records: the lookahead's Gram terms and the
 // label of every row, recomputed per call).
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,

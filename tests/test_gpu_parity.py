@@ -184,11 +184,15 @@ def test_cluster_kernel(orc, name, K, n, epochs):
     assert np.abs(merged - omerged).max() < TOL
 
 
-@pytest.mark.parametrize("kernel", ["resident", "cluster", "reference"])
+@pytest.mark.parametrize("kernel", ["resident", "resident_v8", "cluster", "reference"])
 @pytest.mark.parametrize("rows_per_cn", [1, 2, 3, 4, 5, 6, 17])
-def test_short_slices(orc, kernel, rows_per_cn):
+def test_short_slices(orc, kernel, rows_per_cn, monkeypatch):
     """Slices shorter than the resident kernel's lookahead / prefetch depths (L = 4,
-    8 rows in flight) and the cluster kernel's ring, with one ragged slice."""
+    8 rows in flight) and the cluster kernel's ring, with one ragged slice.  6 CNs fit
+    the GPU, so AUTO's resident plan is v10; resident_v8 forces v8 (PNN_RESIDENT_V10=0)."""
+    if kernel == "resident_v8":
+        monkeypatch.setenv("PNN_RESIDENT_V10", "0")
+        kernel = "resident"
     c = CONFIGS["C4"]
     K = 6
     n = K * rows_per_cn + (1 if rows_per_cn > 1 else 0)
