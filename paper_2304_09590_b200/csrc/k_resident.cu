@@ -87,7 +87,7 @@ constexpr int kTraceT = 64, kTraceP = 16;   // debug timeline: [cta][warp][t][po
 
 struct __align__(16) Smem {
     uint64_t xfull[S];                 // x(u) and its gram record landed
-    uint64_t aready[AR];               // all warps' row sums of sample s (count NW)
+    uint64_t aready[AR];               // all warps' row sums of sample s + the end of chain s-1 (count NW + 2)
     uint64_t gready[GR];               // chain → sweeps: g(c) of every row (the pair: count 2)
     uint64_t zfull[ZS];                // partial logits of sample c from every CTA (count 2 + tx)
     float asum[AR][UMAX][4];           // [s % AR][row][part] partial row sums of acc(s)
@@ -239,10 +239,14 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
-        for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NW);
+        // aready(s): every warp's F(s) and the end of chain s-1 (its pair arrives), so the
+        // chain of s waits once; sample 0 has no previous chain
+        for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NW + 2);
         for (int i = 0; i < GR; ++i) mbar_init(&sm.gready[i], 2);
         for (int i = 0; i < ZS; ++i) mbar_init(&sm.zfull[i], 2);
         fence_mbar_init();
+        mbar_arrive(&sm.aready[0]);
+        mbar_arrive(&sm.aready[0]);
     }
     for (int i = threadIdx.x; i < (S + 1) * DP; i += blockDim.x) xring[i] = 0.f;   // + zero row
     for (int i = threadIdx.x; i < GR * UMAX; i += blockDim.x) (&sm.gbuf[0][0])[i] = 0.f;
@@ -526,8 +530,8 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         if (c >= 0 && c < T && (c % kChainPairs) + (4 - kChainPairs) == (warp >> 1)) {
 #endif
             const int cs = (sx >= 1) ? sx - 1 : S - 1;          // ring slot of x(c)
-            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));   // every warp's row sums of c
-            if (c >= 1) mbar_wait(&sm.gready[(c - 1) % GR], (uint32_t)(((c - 1) / GR) & 1));   // chain c-1
+            // every warp's row sums of c and the end of chain c-1 (W2, b, g history in shared memory)
+            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
             TR(3);
             // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c); h(c) of unit uc ----
             const float4 G = *reinterpret_cast<const float4*>(xring + cs * DP + GOFF);
@@ -681,7 +685,10 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 bq[2] = make_float4(fmaf(-lr, dl[8], b2v.x), fmaf(-lr, dl[9], b2v.y), 0.f, 0.f);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.gready[c % GR]);
+            if (lane == 0) {
+                mbar_arrive(&sm.gready[c % GR]);
+                if (c + 1 < T) mbar_arrive(&sm.aready[(c + 1) % AR]);   // chain c+1 may start
+            }
 #if PNN_SWEEP_XWAIT
             // off the critical path: every warp has passed U(c-1) (aready(c) above), so the
             // slot of x(c-1-L) is free for x(c+PF); the sweeps wait for it themselves
