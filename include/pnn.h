@@ -81,7 +81,15 @@ enum { PNN_FP32 = 0, PNN_BF16 = 1 };
 /* Training kernel selection (pnn_set_kernel). */
 enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          */
        PNN_KERNEL_REFERENCE = 1, /* one CTA per CN, weights in global memory    */
-       PNN_KERNEL_RESIDENT = 2,  /* persistent cluster kernel, on-chip weights  */
+       PNN_KERNEL_RESIDENT = 2,  /* persistent cluster kernel, on-chip weights:
+                                    W1 in registers (2-layer nets, 768 < D <=
+                                    784, O = 10, H <= 256).  Variant v8 (chain
+                                    on rotating warp pairs, 2 SMs per CN at
+                                    H = 128) or v10 (chain on its own CTA, one
+                                    SM more, shorter period): AUTO takes v10
+                                    when all concurrently trained CNs fit the
+                                    GPU (K_local or slots x 3 <= 148, H <= 128);
+                                    environment PNN_RESIDENT_V10=0/1 forces.   */
        PNN_KERNEL_TC_BF16 = 3,   /* bf16 mini-batch on tcgen05 GEMMs; chosen by
                                     pnn_set_minibatch(.., PNN_BF16), reported
                                     by pnn_kernel_info, not settable         */
