@@ -72,3 +72,35 @@ def test_short_and_ragged_slices(orc, rows_per_cn):
     K = 5
     n = K * rows_per_cn + 2
     _run(orc, c.layers, c.act, c.init, K, c.lr, n, 8, epochs=2)
+
+
+def test_f1_full_sampled(orc):
+    """F1 at its full size (60,000 rows, K = 10, 20 epochs, batch 50; the configuration
+    bench.py times) on the resident mini-batch kernel; the oracle re-trains CNs 0 and 9.
+    R22 per-CN rule: < 1e-4, or <= 2x the oracle's 1-ulp perturbation envelope."""
+    from paper_2304_09590_b200 import PNN
+    from tests.envelope import perturbation_envelope
+    c = CONFIGS["F1"]
+    X, y = make_split(c.n_train, "train", 0)
+    net = PNN(c.layers, c.act, c.init, c.K, c.lr, seed=0)
+    net.set_minibatch(c.batch)
+    assert tuple(net.kernel_info()) == (6, 1)
+    xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    for _ in range(c.epochs):
+        net.train_epoch(xd, yd)
+    torch.cuda.synchronize()
+    sample = [0, 9]
+    okids, _ = orc.train_pnn(c.layers, c.act, c.init, c.K, c.lr, 0, X, y, epochs=c.epochs, batch=c.batch,
+                             threads=8, subnets=sample)
+    start, count = orc.shard_bounds(c.n_train, c.K)
+    p0 = orc.init_params(c.layers, c.init, 0)
+    report = []
+    for j, i in enumerate(sample):
+        err = float(np.abs(net.get_params(i) - okids[j]).max())
+        env = None
+        if err >= TOL:
+            a, b = int(start[i]), int(start[i] + count[i])
+            env = perturbation_envelope(orc, c.layers, c.act, p0, X[a:b], y[a:b], c.lr, c.epochs, batch=c.batch)
+        report.append((i, err, env))
+        assert err < TOL or err <= 2 * env, f"CN {i}: max-abs {err:.3g}, fp32 envelope {env}"
+    print("F1 full per-CN (index, max-abs vs oracle, fp32 envelope):", report)
