@@ -410,3 +410,23 @@ def test_c3_full_sampled(orc):
 
 def test_c4_full_sampled(orc):
     _full(orc, "C4", [0, 1, 511, 777, 1023])
+
+
+@pytest.mark.parametrize("name,K,rows,batch", [
+    ("C3", 40, 40 * 12 + 5, 1),      # deep cluster variant, 2 host-copy groups (18 CNs per group)
+    ("F1", 40, 40 * 60 + 7, 50),     # resident mini-batch kernel, 2 groups
+    ("C2", 4, 4 * 100 + 3, 1),       # v10 resident variant
+])
+def test_host_input_path_other_kernels(name, K, rows, batch):
+    """pnn_train_epoch_host (H2D copies pipelined with training in CN groups) gives the
+    device path's parameters bit for bit on the deep, mini-batch and v10 kernels."""
+    c = CONFIGS[name]
+    X, y = make_split(rows, "train", 0)
+    a = _train(c.layers, c.act, c.init, K, c.lr, X, y, batch=batch)[1]
+    net = PNN(c.layers, c.act, c.init, K, c.lr, seed=0)
+    if batch > 1:
+        net.set_minibatch(batch)
+    net.train_epoch_host(torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory())
+    torch.cuda.synchronize()
+    b = np.stack([net.get_params(i) for i in range(K)])
+    np.testing.assert_array_equal(a, b)
