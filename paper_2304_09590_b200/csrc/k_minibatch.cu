@@ -310,7 +310,9 @@ __global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, 
         float zz[16];
 #pragma unroll
         for (int o = 0; o < 16; ++o) zz[o] = 0.f;
-        for (int t = 0; t < nt; ++t) {
+        const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;   // issued early
+#pragma unroll 8
+        for (int t = 0; t < nt; ++t) {                 // (the tiles' loads issue together)
             const float4* zq = reinterpret_cast<const float4*>(s.z3part + (((long long)z * nt + t) * 64 + b) * 16);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -318,7 +320,6 @@ __global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, 
                 zz[4 * q] += f.x; zz[4 * q + 1] += f.y; zz[4 * q + 2] += f.z; zz[4 * q + 3] += f.w;
             }
         }
-        const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;
         float m = -INFINITY;
 #pragma unroll
         for (int o = 0; o < 16; ++o)
