@@ -77,6 +77,14 @@ constexpr bool kV8SameOrder = PNN_V8_SAME_ORDER != 0;
 #ifndef PNN_SWEEP_XWAIT
 #define PNN_SWEEP_XWAIT 1
 #endif
+// paired sweeps: F / U for two samples per pass over the W¹ registers (5 Gram terms)
+#ifndef PNN_V8_PAIRS
+#define PNN_V8_PAIRS 1
+#endif
+#ifndef PNN_V8P_STAGGER
+#define PNN_V8P_STAGGER 0   // warps 4-7 U before F: measured slower (51.7 vs 67.4 M)
+#endif
+constexpr bool kStagger = PNN_V8P_STAGGER != 0;
 // the chain warp of the pair that does not issue the x prefetch updates b2
 constexpr int kB2Half = PNN_SWEEP_XWAIT ? 1 : 0;
 // warp pairs that take turns running the chain: the highest-numbered ones (the warp
@@ -130,7 +138,7 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
 
 // Gram record of every row of CNs [s_first, s_first + s_count) (shard-local index u):
 // rec[2·row] = {x(u-4)·x(u), x(u-3)·x(u), x(u-2)·x(u), x(u-1)·x(u)} (0 before the slice
-// start), rec[2·row + 1] = {label bits, 0, 0, 0}.  A warp walks a chunk of GCH consecutive
+// start), rec[2·row + 1] = {label bits, x(u-5)·x(u), 0, 0}.  A warp walks a chunk of GCH consecutive
 // rows keeping the last four rows in registers (lane l: columns 4l + 128q, q < 6, and
 // 768 + 4l for l < 4), so X is read from HBM about once.
 constexpr int GCH = 32;
@@ -168,11 +176,11 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
     const long long nchunks = (rows + GCH - 1) / GCH;
     for (long long ch = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
         const long long a0 = r0 + ch * GCH, a1 = min(a0 + GCH, r0 + rows);
-        float4 win[4][7];                          // win[k] = x(row - 4 + k), k = 0..3
+        float4 win[5][7];                          // win[k] = x(row - 5 + k), k = 0..4
         const long long st = shard_start(a0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const long long pr = a0 - 4 + k;
+        for (int k = 0; k < 5; ++k) {
+            const long long pr = a0 - 5 + k;
             if (pr >= st) load(pr, win[k]);
             else
 #pragma unroll
@@ -184,7 +192,7 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
             const long long s0 = shard_start(row);
             if (s0 == row && row != a0) {          // a new slice begins: no terms before it
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < 5; ++k)
 #pragma unroll
                     for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
@@ -192,19 +200,19 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
 #pragma unroll
             for (int q = 0; q < 7; ++q) cur[q] = nxt[q];
             if (row + 1 < a1) load(row + 1, nxt);  // one row ahead
-            float gk[4];
+            float gk[5];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) gk[k] = warp_sum(dot(win[k], cur));
-            if (lane == 0) {
-                rec[2 * row] = make_float4(gk[0], gk[1], gk[2], gk[3]);
-                rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), 0.f, 0.f, 0.f);
+            for (int k = 0; k < 5; ++k) gk[k] = warp_sum(dot(win[k], cur));
+            if (lane == 0) {                       // {G(u-4..u-1)}, {label, G(u-5)} (the paired sweeps' 5th term)
+                rec[2 * row] = make_float4(gk[1], gk[2], gk[3], gk[4]);
+                rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), gk[0], 0.f, 0.f);
             }
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
+            for (int k = 0; k < 4; ++k)
 #pragma unroll
                 for (int q = 0; q < 7; ++q) win[k][q] = win[k + 1][q];
 #pragma unroll
-            for (int q = 0; q < 7; ++q) win[3][q] = cur[q];
+            for (int q = 0; q < 7; ++q) win[4][q] = cur[q];
         }
     }
 }
@@ -321,6 +329,334 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     constexpr uint32_t kZStride = 2 * CMAX * 16 * 4;
     constexpr uint32_t kZfullOff = (uint32_t)offsetof(Smem, zfull) - (uint32_t)offsetof(Smem, zbuf);
 
+#if PNN_V8_PAIRS
+    // ===== paired sweeps: step p runs F for samples 2p, 2p+1 with W¹(2p-L) (one pass over the
+    // registers for both: 32 fma.rn.f32x2 per pair of x quads), U for samples 2p-4, 2p-3, and
+    // the chains of samples 2p-2, 2p-1 on their warp pairs.  Sample 2p+1's forward misses
+    // the updates of 2p-4 .. 2p (5 Gram corrections; even samples 4). =====
+    const int npair = (T + 1) >> 1;
+    auto u_pair = [&](int p) {
+    if (p >= 2 && 2 * (p - 2) < T) {
+        // ---------------- U(2p-4), U(2p-3): W¹ -= g(u)·x(u)ᵀ in sample order ----------------
+        const int u0 = 2 * (p - 2), u1 = u0 + 1;
+        const bool v1 = u1 < T;
+        const int ul = v1 ? u1 : u0;           // chain u1 done ⇒ chain u0 done
+        mbar_wait(&sm.gready[ul % GR], (uint32_t)((ul / GR) & 1));
+        const int sl0 = u0 % S, sl1 = v1 ? u1 % S : S;
+        const float* xo0 = xring + sl0 * DP + 4 * lane;
+        const float* xo1 = xring + sl1 * DP + 4 * lane;
+        float gp0[R], gp1[R];
+        {
+            const float4* g0v = reinterpret_cast<const float4*>(&sm.gbuf[u0 % GR][kr0]);
+            const float4* g1v = reinterpret_cast<const float4*>(&sm.gbuf[u1 % GR][kr0]);
+            const float4 a0 = g0v[0], a1 = g0v[1];
+            float4 c0 = g1v[0], c1 = g1v[1];
+            if (!v1) { c0 = make_float4(0.f, 0.f, 0.f, 0.f); c1 = c0; }
+            gp0[0] = -a0.x; gp0[1] = -a0.y; gp0[2] = -a0.z; gp0[3] = -a0.w;
+            gp0[4] = -a1.x; gp0[5] = -a1.y; gp0[6] = -a1.z; gp0[7] = -a1.w;
+            gp1[0] = -c0.x; gp1[1] = -c0.y; gp1[2] = -c0.z; gp1[3] = -c0.w;
+            gp1[4] = -c1.x; gp1[5] = -c1.y; gp1[6] = -c1.z; gp1[7] = -c1.w;
+        }
+        uint64_t xa, xb, ya, yb;
+        lds4(xo0, xa, xb);
+        lds4(xo1, ya, yb);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            uint64_t na = 0ull, nb = 0ull, ma = 0ull, mb = 0ull;
+            if (q + 1 < NQ) {
+                lds4(xo0 + 128 * (q + 1), na, nb);
+                lds4(xo1 + 128 * (q + 1), ma, mb);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                w[r][2 * q] = ffma2(pk(gp0[r], gp0[r]), xa, w[r][2 * q]);
+                w[r][2 * q + 1] = ffma2(pk(gp0[r], gp0[r]), xb, w[r][2 * q + 1]);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                w[r][2 * q] = ffma2(pk(gp1[r], gp1[r]), ya, w[r][2 * q]);
+                w[r][2 * q + 1] = ffma2(pk(gp1[r], gp1[r]), yb, w[r][2 * q + 1]);
+            }
+            xa = na; xb = nb; ya = ma; yb = mb;
+        }
+        __syncwarp();                          // F's tail reads of wx are done
+        float4 w4 = *reinterpret_cast<const float4*>(wxp);
+        const float4 x4 = *reinterpret_cast<const float4*>(xring + sl0 * DP + XC + 4 * tq);
+        const float4 y4 = *reinterpret_cast<const float4*>(xring + sl1 * DP + XC + 4 * tq);
+        const float g0 = -sm.gbuf[u0 % GR][kr0 + tr], g1 = v1 ? -sm.gbuf[u1 % GR][kr0 + tr] : 0.f;
+        w4.x = fmaf(g0, x4.x, w4.x); w4.y = fmaf(g0, x4.y, w4.y);
+        w4.z = fmaf(g0, x4.z, w4.z); w4.w = fmaf(g0, x4.w, w4.w);
+        w4.x = fmaf(g1, y4.x, w4.x); w4.y = fmaf(g1, y4.y, w4.y);
+        w4.z = fmaf(g1, y4.z, w4.z); w4.w = fmaf(g1, y4.w, w4.w);
+        *reinterpret_cast<float4*>(wxp) = w4;
+    }
+    };
+
+    const int trow = lane >> 2, tsmp = (lane >> 1) & 1, th8 = lane & 1;   // F's tail: row, sample, 8 columns
+    for (int p = 0; p < npair + 3; ++p) {
+        const int s = 2 * p;                       // (TR's index)
+        TR(0);
+        __syncwarp();
+        if (kStagger && warp >= 4) u_pair(p);
+        __syncwarp();
+        if (p < npair) {
+            // ---------------- F(2p), F(2p+1) ----------------
+            const int s0 = 2 * p, s1 = 2 * p + 1;
+            const bool v1 = s1 < T;
+            const int sl0 = s0 % S, sl1 = v1 ? s1 % S : S;   // slot S: the zero row
+            mbar_wait(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
+            if (v1) mbar_wait(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
+            const float* xn0 = xring + sl0 * DP + 4 * lane;
+            const float* xn1 = xring + sl1 * DP + 4 * lane;
+            uint64_t acc0[R], acc1[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
+            uint64_t xa, xb, ya, yb;
+            lds4(xn0, xa, xb);
+            lds4(xn1, ya, yb);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t na = 0ull, nb = 0ull, ma = 0ull, mb = 0ull;
+                if (q + 1 < NQ) {
+                    lds4(xn0 + 128 * (q + 1), na, nb);
+                    lds4(xn1 + 128 * (q + 1), ma, mb);
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc0[r] = ffma2(w[r][2 * q], xa, acc0[r]);
+                    acc1[r] = ffma2(w[r][2 * q], ya, acc1[r]);
+                    acc0[r] = ffma2(w[r][2 * q + 1], xb, acc0[r]);
+                    acc1[r] = ffma2(w[r][2 * q + 1], yb, acc1[r]);
+                }
+                xa = na; xb = nb; ya = ma; yb = mb;
+            }
+            float px;                              // row trow, sample tsmp, columns 768 + 8·th8 .. +7
+            {
+                const float* wt = &sm.wx[warp][trow][8 * th8];
+                const float* xt = xring + (tsmp ? sl1 : sl0) * DP + XC + 8 * th8;
+                const float4 w0 = *reinterpret_cast<const float4*>(wt), w1 = *reinterpret_cast<const float4*>(wt + 4);
+                const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
+                px = w0.x * x0.x;
+                px = fmaf(w0.y, x0.y, px); px = fmaf(w0.z, x0.z, px); px = fmaf(w0.w, x0.w, px);
+                px = fmaf(w1.x, x1.x, px); px = fmaf(w1.y, x1.y, px); px = fmaf(w1.z, x1.z, px);
+                px = fmaf(w1.w, x1.w, px);
+            }
+            float v[16];                           // v[2r + sample]
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float lo, hi;
+                upk(acc0[r], lo, hi);
+                v[2 * r] = lo + hi;
+                upk(acc1[r], lo, hi);
+                v[2 * r + 1] = lo + hi;
+            }
+            // transpose-reduce 16 values: lane l ends with v[l >> 1] = (row l >> 2, sample (l >> 1) & 1)
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+            float u8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                u8[i] = (b4 ? v[i + 8] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 8], 16);
+            float u4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                u4[i] = (b3 ? u8[i + 4] : u8[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u8[i] : u8[i + 4], 8);
+            float u2[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                u2[i] = (b2 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b2 ? u4[i] : u4[i + 2], 4);
+            float zsum = (b1 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? u2[0] : u2[1], 2) + px;
+            zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
+            if (th8 == 0 && (tsmp == 0 || v1))
+                *reinterpret_cast<float4*>(&sm.asum[(tsmp ? s1 : s0) % AR][kr0 + trow][0]) =
+                    make_float4(zsum, 0.f, 0.f, 0.f);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&sm.aready[s0 % AR]);
+                if (v1) mbar_arrive(&sm.aready[s1 % AR]);
+            }
+        }
+        TR(1);
+        // ================= the chains of samples 2p-2, 2p-1 (one warp pair each) =================
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * p - 2 + cc;
+        if (c >= 0 && c < T && (c % kChainPairs) + (4 - kChainPairs) == (warp >> 1)) {
+            const int cs = c % S;                  // ring slot of x(c)
+            // every warp's row sums of c and the end of chain c-1 (W2, b, g history in shared memory)
+            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
+            TR(3);
+            // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c), k = 1..4 (+5 for odd c); h(c) of unit uc ----
+            const float4 G = *reinterpret_cast<const float4*>(xring + cs * DP + GOFF);
+            const int label = __float_as_int(xring[cs * DP + GOFF + 4]);
+            const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][uc][0]);
+            float z = (pa.x + pa.y) + (pa.z + pa.w);
+            // F-before-U rows (warps 0-3: half 0) miss 4 (+1 odd) updates, U-first rows 2 (+1 odd)
+            const bool fu = !kStagger || half == 0;
+            if (fu && (c & 1)) z = fmaf(-sm.gbuf[(c + GR - 5) % GR][uc], xring[cs * DP + GOFF + 5], z);
+            if (fu) z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);
+            if (fu || (c & 1)) z = fmaf(-sm.gbuf[(c + GR - 3) % GR][uc], G.y, z);
+            z = fmaf(-sm.gbuf[(c + GR - 2) % GR][uc], G.z, z);
+            z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
+            z += sm.b1s[uc];
+            const float h = lc ? act_fwd_t<A1>(z) : 0.f;
+            TR(7);
+            // W2[o][uc] (pre-update: R6), kept for δ1 below
+            float wv[12];
+            const int zs = c % ZS;
+            {
+                const float4* wq = reinterpret_cast<const float4*>(&sm.w2s[uc][0]);
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float4 f = wq[q];
+                    wv[4 * q] = f.x; wv[4 * q + 1] = f.y; wv[4 * q + 2] = f.z; wv[4 * q + 3] = f.w;
+                }
+            }
+            // ---- this warp's partial logits Σ_u W2[o][u] h_u: transpose-reduce over lanes ----
+            float pv0;
+            {
+                float pv[16];
+#pragma unroll
+                for (int o = 0; o < 16; ++o) pv[o] = (o < O) ? wv[o < O ? o : 0] * h : 0.f;
+                const bool c4 = lane & 16, c3 = lane & 8, c2 = lane & 4, c1 = lane & 2;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    pv[i] = (c4 ? pv[i + 8] : pv[i]) + __shfl_xor_sync(0xffffffffu, c4 ? pv[i] : pv[i + 8], 16);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    pv[i] = (c3 ? pv[i + 4] : pv[i]) + __shfl_xor_sync(0xffffffffu, c3 ? pv[i] : pv[i + 4], 8);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    pv[i] = (c2 ? pv[i + 2] : pv[i]) + __shfl_xor_sync(0xffffffffu, c2 ? pv[i] : pv[i + 2], 4);
+                pv0 = (c1 ? pv[1] : pv[0]) + __shfl_xor_sync(0xffffffffu, c1 ? pv[0] : pv[1], 2);
+                pv0 += __shfl_xor_sync(0xffffffffu, pv0, 1);
+            }
+            TR(8);
+            // lane l now holds output (l >> 1) = 8·c4 + 4·c3 + 2·c2 + c1
+            {
+                const int oi = lane >> 1;
+                const bool pub = (lane & 1) == 0 && oi < O;
+                if (pub) sm.zbuf[zs][zrow][oi] = pv0;
+                if constexpr (C > 1) {
+#pragma unroll
+                    for (int p = 0; p < C - 1; ++p)
+                        st_async_f32_if(pub, rz[p] + zs * kZStride + oi * 4, pv0,
+                                        rz[p] + kZfullOff - (uint32_t)(zrow * 64) + zs * 8);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (C > 1) mbar_arrive_expect_tx(&sm.zfull[zs], (uint32_t)((C - 1) * O * 4));
+                    else mbar_arrive(&sm.zfull[zs]);
+                }
+            }
+            TR(9);
+            // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
+            //      which comes after their wait on gready(c) (first warp of the pair) ----
+            // every warp has passed U(c-1) (aready(c) above): the slot of x(c-1-L) is free for x(c+PF)
+#if !PNN_SWEEP_XWAIT
+            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
+            if (half == 0 && c + 2 + LAG < T) {
+                const int u = c + 2 + LAG;
+                mbar_wait(&sm.xfull[(cs + 2 + LAG) % S], (uint32_t)((u / S) & 1));
+            }
+#endif
+            TR(4);
+            // ---- δ2(c) in every lane: z2 = Σ partials + b2(c) ----
+            mbar_wait(&sm.zfull[zs], (uint32_t)((c / ZS) & 1));
+            TR(5);
+            float dl[O];
+            {
+                float z2[12];
+                {
+                    const float4* bq = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const float4 f = bq[q];
+                        z2[4 * q] = f.x; z2[4 * q + 1] = f.y; z2[4 * q + 2] = f.z; z2[4 * q + 3] = f.w;
+                    }
+                }
+                float zp[12];
+#pragma unroll
+                for (int o = 0; o < 12; ++o) zp[o] = 0.f;
+#pragma unroll
+                for (int i = 0; i < 2 * C; ++i) {
+                    const float4* zq = reinterpret_cast<const float4*>(&sm.zbuf[zs][i][0]);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const float4 f = zq[q];
+                        zp[4 * q] += f.x; zp[4 * q + 1] += f.y; zp[4 * q + 2] += f.z; zp[4 * q + 3] += f.w;
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < 12; ++o) z2[o] += zp[o];                // z2 = W2 h + b2 (Eq.2)
+                if constexpr (A2 == PNN_SOFTMAX) {
+                    // max and sum as trees (O = 10: depth 4 instead of 9)
+                    const float m = fmaxf(fmaxf(fmaxf(z2[0], z2[1]), fmaxf(z2[2], z2[3])),
+                                          fmaxf(fmaxf(fmaxf(z2[4], z2[5]), fmaxf(z2[6], z2[7])), fmaxf(z2[8], z2[9])));
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = __expf(z2[o] - m);
+                    const float sum = ((dl[0] + dl[1]) + (dl[2] + dl[3])) +
+                                      (((dl[4] + dl[5]) + (dl[6] + dl[7])) + (dl[8] + dl[9]));
+                    float inv;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
+                    TR(10);
+                } else {
+                    // element-wise output (sigmoid / tanh, ½-SSE: Eq.9, R11): lane o forms output
+                    // o's activation and δ2 once, then every lane takes the ten by shuffles
+                    float zsel = z2[0];
+#pragma unroll
+                    for (int o = 1; o < O; ++o) zsel = (lane == o) ? z2[o] : zsel;
+                    const float x2 = act_fwd_t<A2>(zsel);
+                    const float dmine = (x2 - ((lane == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
+#pragma unroll
+                    for (int o = 0; o < O; ++o) dl[o] = __shfl_sync(0xffffffffu, dmine, o);
+                }
+            }
+            // ---- δ1, g(c) of unit uc; W2(c+1), b1(c+1), b2(c+1) ----
+            {
+                float s1 = 0.f;                    // (W2ᵀδ2)_u with the pre-update W2 (R6)
+#pragma unroll
+                for (int o = 0; o < O; ++o) s1 = fmaf(wv[o], dl[o], s1);
+                const float gu = lc ? lr * (s1 * act_deriv_t<A1>(h)) : 0.f;   // g(c) = η δ1
+                sm.gbuf[c % GR][uc] = gu;
+                TR(11);
+                sm.b1s[uc] -= gu;
+#pragma unroll
+                for (int o = 0; o < O; ++o) wv[o] = fmaf(-(lr * dl[o]), h, wv[o]);
+                float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
+                wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+                wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
+                wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
+            }
+            if (half == kB2Half && lane == 0) {        // b2(c+1) into the other buffer: the pair's
+                const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);   // partner may
+                float4* bq = reinterpret_cast<float4*>(&sm.b2s[(c + 1) & 1][0]);        // still read b2(c)
+                const float4 b0 = bo[0], b1v = bo[1], b2v = bo[2];
+                bq[0] = make_float4(fmaf(-lr, dl[0], b0.x), fmaf(-lr, dl[1], b0.y), fmaf(-lr, dl[2], b0.z),
+                                    fmaf(-lr, dl[3], b0.w));
+                bq[1] = make_float4(fmaf(-lr, dl[4], b1v.x), fmaf(-lr, dl[5], b1v.y), fmaf(-lr, dl[6], b1v.z),
+                                    fmaf(-lr, dl[7], b1v.w));
+                bq[2] = make_float4(fmaf(-lr, dl[8], b2v.x), fmaf(-lr, dl[9], b2v.y), 0.f, 0.f);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&sm.gready[c % GR]);
+                if (c + 1 < T) mbar_arrive(&sm.aready[(c + 1) % AR]);   // chain c+1 may start
+            }
+#if PNN_SWEEP_XWAIT
+            // off the critical path: every warp has passed U(c-1) (aready(c) above), so the
+            // slot of x(c-1-L) is free for x(c+PF); the sweeps wait for it themselves
+            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
+#endif
+            TR(6);
+        }
+        }
+        // U after the chains: a chain then starts right after its warps' F (warps 4-7, the
+        // sub-partition partners of 0-3, run U first: out of phase, 2 / 3 corrections)
+        if (!kStagger || warp < 4) u_pair(p);
+    }
+#else
     int sx = 0;                                    // ring slot of x(s) = s % S
     for (int s = 0; s <= T + LAG; ++s) {
         TR(0);
@@ -698,6 +1034,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         }
         if (++sx == S) sx = 0;
     }
+#endif
 #undef TR
 
     // ---- write back ----
