@@ -357,16 +357,11 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             gp1[0] = -c0.x; gp1[1] = -c0.y; gp1[2] = -c0.z; gp1[3] = -c0.w;
             gp1[4] = -c1.x; gp1[5] = -c1.y; gp1[6] = -c1.z; gp1[7] = -c1.w;
         }
-        uint64_t xa, xb, ya, yb;
-        lds4(xo0, xa, xb);
-        lds4(xo1, ya, yb);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            uint64_t na = 0ull, nb = 0ull, ma = 0ull, mb = 0ull;
-            if (q + 1 < NQ) {
-                lds4(xo0 + 128 * (q + 1), na, nb);
-                lds4(xo1 + 128 * (q + 1), ma, mb);
-            }
+            uint64_t xa, xb, ya, yb;
+            lds4(xo0 + 128 * q, xa, xb);
+            lds4(xo1 + 128 * q, ya, yb);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 w[r][2 * q] = ffma2(pk(gp0[r], gp0[r]), xa, w[r][2 * q]);
@@ -377,7 +372,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 w[r][2 * q] = ffma2(pk(gp1[r], gp1[r]), ya, w[r][2 * q]);
                 w[r][2 * q + 1] = ffma2(pk(gp1[r], gp1[r]), yb, w[r][2 * q + 1]);
             }
-            xa = na; xb = nb; ya = ma; yb = mb;
         }
         __syncwarp();                          // F's tail reads of wx are done
         float4 w4 = *reinterpret_cast<const float4*>(wxp);
@@ -411,16 +405,11 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             uint64_t acc0[R], acc1[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
-            uint64_t xa, xb, ya, yb;
-            lds4(xn0, xa, xb);
-            lds4(xn1, ya, yb);
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                uint64_t na = 0ull, nb = 0ull, ma = 0ull, mb = 0ull;
-                if (q + 1 < NQ) {
-                    lds4(xn0 + 128 * (q + 1), na, nb);
-                    lds4(xn1 + 128 * (q + 1), ma, mb);
-                }
+            for (int q = 0; q < NQ; ++q) {             // 32 FFMA2 per quad pair cover the loads
+                uint64_t xa, xb, ya, yb;
+                lds4(xn0 + 128 * q, xa, xb);
+                lds4(xn1 + 128 * q, ya, yb);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     acc0[r] = ffma2(w[r][2 * q], xa, acc0[r]);
@@ -428,7 +417,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                     acc0[r] = ffma2(w[r][2 * q + 1], xb, acc0[r]);
                     acc1[r] = ffma2(w[r][2 * q + 1], yb, acc1[r]);
                 }
-                xa = na; xb = nb; ya = ma; yb = mb;
             }
             float px;                              // row trow, sample tsmp, columns 768 + 8·th8 .. +7
             {
