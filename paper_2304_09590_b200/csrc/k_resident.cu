@@ -1069,6 +1069,12 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 // every sweep warp runs F then U (one code stream per SM sub-partition) instead of the
 // v8 phase shift (warps 4..7: U then F)
 constexpr bool kSplitSameOrder = PNN_SPLIT_SAME_ORDER != 0;
+// paired sweeps (as v8's PNN_V8_PAIRS): F / U for two samples per pass, one complete row sum
+// per unit sent to the chain CTA, 5 Gram corrections for odd samples
+#ifndef PNN_SPLIT_PAIRS
+#define PNN_SPLIT_PAIRS 1
+#endif
+constexpr bool kSplitPairs = PNN_SPLIT_PAIRS != 0;
 constexpr int RS = 16;               // chain CTA: Gram-record ring slots
 constexpr int RPF = 8;               // records in flight
 constexpr int SPF = S - 2 * LAG - 1; // sweep CTAs: x prefetch distance (slot provably free, see below)
@@ -1129,7 +1135,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             mbar_arrive_expect_tx(&sm.xfull[slot], xbytes);
             bulk_g2s(xring + slot * DP, Xc + (long long)u * D, xbytes, &sm.xfull[slot]);
         };
-        for (int i = threadIdx.x; i < S * DP; i += blockDim.x) xring[i] = 0.f;
+        for (int i = threadIdx.x; i < (S + 1) * DP; i += blockDim.x) xring[i] = 0.f;   // + zero row
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0)
@@ -1252,6 +1258,136 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             *reinterpret_cast<float4*>(wxp) = w4;
         };
 
+        if constexpr (kSplitPairs) {
+        const int trow = lane >> 2, tsmp = (lane >> 1) & 1, th8 = lane & 1;
+        const bool rlive = kr0 + trow < Uown;
+        const uint32_t apart0 = mapa(smem_u32(&sm.asum[0][k0 + kr0 + trow][0]), (uint32_t)NSW);
+        auto sweep_f2 = [&](int s0, bool v1) {
+            const int s1 = s0 + 1;
+            const int sl0 = s0 % S, sl1 = v1 ? s1 % S : S;    // slot S: the zero row
+            mbar_wait(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
+            if (v1) mbar_wait(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
+            const float* xn0 = xring + sl0 * DP + 4 * lane;
+            const float* xn1 = xring + sl1 * DP + 4 * lane;
+            uint64_t acc0[R], acc1[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t xa, xb, ya, yb;
+                lds4(xn0 + 128 * q, xa, xb);
+                lds4(xn1 + 128 * q, ya, yb);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc0[r] = ffma2(w[r][2 * q], xa, acc0[r]);
+                    acc1[r] = ffma2(w[r][2 * q], ya, acc1[r]);
+                    acc0[r] = ffma2(w[r][2 * q + 1], xb, acc0[r]);
+                    acc1[r] = ffma2(w[r][2 * q + 1], yb, acc1[r]);
+                }
+            }
+            float px;
+            {
+                const float* wt = &sm.wx[warp][trow][8 * th8];
+                const float* xt = xring + (tsmp ? sl1 : sl0) * DP + XC + 8 * th8;
+                const float4 w0 = *reinterpret_cast<const float4*>(wt), w1 = *reinterpret_cast<const float4*>(wt + 4);
+                const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
+                px = w0.x * x0.x;
+                px = fmaf(w0.y, x0.y, px); px = fmaf(w0.z, x0.z, px); px = fmaf(w0.w, x0.w, px);
+                px = fmaf(w1.x, x1.x, px); px = fmaf(w1.y, x1.y, px); px = fmaf(w1.z, x1.z, px);
+                px = fmaf(w1.w, x1.w, px);
+            }
+            float v[16];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float lo, hi;
+                upk(acc0[r], lo, hi);
+                v[2 * r] = lo + hi;
+                upk(acc1[r], lo, hi);
+                v[2 * r + 1] = lo + hi;
+            }
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+            float u8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                u8[i] = (b4 ? v[i + 8] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 8], 16);
+            float u4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                u4[i] = (b3 ? u8[i + 4] : u8[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u8[i] : u8[i + 4], 8);
+            float u2[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+                u2[i] = (b2 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b2 ? u4[i] : u4[i + 2], 4);
+            float zsum = (b1 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? u2[0] : u2[1], 2) + px;
+            zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
+            const int a = (tsmp ? s1 : s0) % AR;
+            st_async_f32_if(rlive && th8 == 0 && (tsmp == 0 || v1), apart0 + (uint32_t)a * kAStride, zsum,
+                            abar + (uint32_t)a * 8u);
+        };
+        auto sweep_u2 = [&](int u0, bool v1) {
+            const int u1 = u0 + 1;
+            mbar_wait(&sm.gready[u0 % GR], (uint32_t)((u0 / GR) & 1));
+            if (v1) mbar_wait(&sm.gready[u1 % GR], (uint32_t)((u1 / GR) & 1));
+            const int sl0 = u0 % S, sl1 = v1 ? u1 % S : S;
+            const float* xo0 = xring + sl0 * DP + 4 * lane;
+            const float* xo1 = xring + sl1 * DP + 4 * lane;
+            float gp0[R], gp1[R];
+            {
+                const float4* g0v = reinterpret_cast<const float4*>(&sm.gbuf[u0 % GR][kr0]);
+                const float4* g1v = reinterpret_cast<const float4*>(&sm.gbuf[u1 % GR][kr0]);
+                const float4 a0 = g0v[0], a1 = g0v[1];
+                float4 c0 = g1v[0], c1 = g1v[1];
+                if (!v1) { c0 = make_float4(0.f, 0.f, 0.f, 0.f); c1 = c0; }
+                gp0[0] = -a0.x; gp0[1] = -a0.y; gp0[2] = -a0.z; gp0[3] = -a0.w;
+                gp0[4] = -a1.x; gp0[5] = -a1.y; gp0[6] = -a1.z; gp0[7] = -a1.w;
+                gp1[0] = -c0.x; gp1[1] = -c0.y; gp1[2] = -c0.z; gp1[3] = -c0.w;
+                gp1[4] = -c1.x; gp1[5] = -c1.y; gp1[6] = -c1.z; gp1[7] = -c1.w;
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint64_t xa, xb, ya, yb;
+                lds4(xo0 + 128 * q, xa, xb);
+                lds4(xo1 + 128 * q, ya, yb);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    w[r][2 * q] = ffma2(pk(gp0[r], gp0[r]), xa, w[r][2 * q]);
+                    w[r][2 * q + 1] = ffma2(pk(gp0[r], gp0[r]), xb, w[r][2 * q + 1]);
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    w[r][2 * q] = ffma2(pk(gp1[r], gp1[r]), ya, w[r][2 * q]);
+                    w[r][2 * q + 1] = ffma2(pk(gp1[r], gp1[r]), yb, w[r][2 * q + 1]);
+                }
+            }
+            __syncwarp();                          // F's tail reads of wx are done
+            float4 w4 = *reinterpret_cast<const float4*>(wxp);
+            const float4 x4 = *reinterpret_cast<const float4*>(xring + sl0 * DP + XC + 4 * tq);
+            const float4 y4 = *reinterpret_cast<const float4*>(xring + sl1 * DP + XC + 4 * tq);
+            const float ga = -sm.gbuf[u0 % GR][kr0 + tr], gb = v1 ? -sm.gbuf[u1 % GR][kr0 + tr] : 0.f;
+            w4.x = fmaf(ga, x4.x, w4.x); w4.y = fmaf(ga, x4.y, w4.y);
+            w4.z = fmaf(ga, x4.z, w4.z); w4.w = fmaf(ga, x4.w, w4.w);
+            w4.x = fmaf(gb, y4.x, w4.x); w4.y = fmaf(gb, y4.y, w4.y);
+            w4.z = fmaf(gb, y4.z, w4.z); w4.w = fmaf(gb, y4.w, w4.w);
+            *reinterpret_cast<float4*>(wxp) = w4;
+            __syncwarp();
+        };
+        const int npair = (T + 1) >> 1;
+        for (int p = 0; p < npair + 2; ++p) {
+            const int s0 = 2 * p;
+            if (threadIdx.x == 0) {                // g(2p), g(2p+1) of this CTA's rows will arrive
+                if (s0 < T) mbar_arrive_expect_tx(&sm.gready[s0 % GR], 4u * (uint32_t)Uown);
+                if (s0 + 1 < T) mbar_arrive_expect_tx(&sm.gready[(s0 + 1) % GR], 4u * (uint32_t)Uown);
+            }
+            if (p < npair) sweep_f2(s0, s0 + 1 < T);
+            if (p >= 2 && 2 * (p - 2) < T) sweep_u2(2 * (p - 2), 2 * (p - 2) + 1 < T);
+            // x(2p+SPF), x(2p+1+SPF) go to the slots of x(2p-9), x(2p-8): thread 0 waited
+            // gready(2p-3) above, so every warp sent its F parts of 2p-3, after its U of ≤ 2p-5
+            if (threadIdx.x == 0) {
+                if (s0 + SPF < T) issue_x(s0 + SPF);
+                if (s0 + 1 + SPF < T) issue_x(s0 + 1 + SPF);
+            }
+        }
+        } else {
         int sx = 0;                                // ring slot of x(s)
         for (int s = 0; s < T + LAG; ++s) {
             // g(s) of this CTA's rows will arrive from the chain CTA: post the expected bytes
@@ -1269,6 +1405,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 if (do_f) sweep_f(s, sx);
             }
             if (++sx == S) sx = 0;
+        }
         }
 #ifdef PNN_SPLIT_PROFILE
         if (blockIdx.x == 0 && lane == 0)
@@ -1298,7 +1435,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
         const bool lc = u < H;
         const int sr = lc ? u / U : 0;             // owning sweep CTA and its row
         const int r = u - sr * U;
-        const bool four = kSplitSameOrder || r < 32;   // rows of warps running F before U
+        const bool four = kSplitPairs || kSplitSameOrder || r < 32;   // rows of warps running F before U
         float w2[O], b2[O];
 #pragma unroll
         for (int o = 0; o < O; ++o) {
@@ -1306,7 +1443,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             b2[o] = b2g[o];
         }
         float b1 = lc ? b1g[u] : 0.f;
-        float g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f;   // g(c-1) .. g(c-4) of this unit
+        float g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f;   // g(c-1) .. g(c-5) of this unit
         const uint32_t gdst = mapa(smem_u32(&sm.gbuf[0][r]), (uint32_t)sr);
         const uint32_t gbar = mapa(smem_u32(&sm.gready[0]), (uint32_t)sr);
         const float4* Rc = rec + 2 * row0;
@@ -1322,7 +1459,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
 #endif
         for (int c = 0; c < T; ++c) {
             if (threadIdx.x == 0) {
-                mbar_arrive_expect_tx(&sm.aready[c % AR], 16u * (uint32_t)H);   // 4 parts of every unit
+                mbar_arrive_expect_tx(&sm.aready[c % AR], (kSplitPairs ? 4u : 16u) * (uint32_t)H);   // parts of every unit
                 if (c + RPF < T) issue_rec(c + RPF);      // its slot held rec(c+RPF-RS): consumed
             }
             mbar_wait(&sm.rfull[c % RS], (uint32_t)((c / RS) & 1));
@@ -1337,7 +1474,8 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
 #endif
             // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c) (R27), h(c) ----
             const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][u][0]);
-            float z = (pa.x + pa.y) + (pa.z + pa.w);
+            float z = kSplitPairs ? pa.x : (pa.x + pa.y) + (pa.z + pa.w);
+            if (kSplitPairs && (c & 1)) z = fmaf(-g5, sm.rec[c % RS][1].y, z);
             if (four) z = fmaf(-g4, G.x, z);
             z = fmaf(-g3, G.y, z);
             z = fmaf(-g2, G.z, z);
@@ -1415,7 +1553,7 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 w2[o] = fmaf(-(lr * dl[o]), h, w2[o]);
                 b2[o] = fmaf(-lr, dl[o], b2[o]);
             }
-            g4 = g3; g3 = g2; g2 = g1; g1 = gu;
+            g5 = g4; g4 = g3; g3 = g2; g2 = g1; g1 = gu;
         }
 #ifdef PNN_SPLIT_PROFILE
         if (blockIdx.x == NSW && lane == 0)
@@ -1563,11 +1701,12 @@ ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent) {
     // PNN_RESIDENT_V10=1 / =0 force it on / off.
     const char* v10 = getenv("PNN_RESIDENT_V10");
     const int c10 = (H + UMAX - 1) / UMAX + 1;
-    const bool want10 = v10 && v10[0] ? v10[0] == '1' : (concurrent > 0 && (long long)concurrent * c10 <= 148);
+    // (≤ 120 SMs: 3-CTA clusters do not all fit 148 SMs at once; K = 48 measured slower than v8)
+    const bool want10 = v10 && v10[0] ? v10[0] == '1' : (concurrent > 0 && (long long)concurrent * c10 <= 120);
     if (H <= 2 * UMAX && want10) {
         p.variant = 10;
         p.cluster = (H + UMAX - 1) / UMAX + 1;
-        p.smem = kSplitHead + sizeof(float) * (size_t)S * DP;
+        p.smem = kSplitHead + sizeof(float) * (size_t)(S + 1) * DP;   // + the zero row (paired sweeps)
     }
     p.ok = true;
     return p;
