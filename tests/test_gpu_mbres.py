@@ -74,6 +74,7 @@ def test_short_and_ragged_slices(orc, rows_per_cn):
     _run(orc, c.layers, c.act, c.init, K, c.lr, n, 8, epochs=2)
 
 
+@pytest.mark.slow
 def test_f1_full_sampled(orc):
     """F1 at its full size (60,000 rows, K = 10, 20 epochs, batch 50; the configuration
     bench.py times) on the resident mini-batch kernel; the oracle re-trains CNs 0 and 9.
