@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "reference", "resident", "cluster"])
+    ap.add_argument("--variant", default="auto",
+                    choices=["auto", "v8", "v10", "tmem", "cluster", "deep", "mb_step", "mb_resident"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -204,6 +206,8 @@ def main():
     net.set_kernel(args.kernel)
     if cfg.batch > 1:
         net.set_minibatch(cfg.batch, PNN_BF16 if cfg.precision == "bf16" else 0)
+    if args.variant != "auto":
+        net.set_variant(args.variant)
     if world > 1:
         net.set_comm(world, rank, nccl_unique_id_bytes(rank))
     kernel_id, launches_per_epoch = net.kernel_info()

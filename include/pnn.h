@@ -81,15 +81,17 @@ enum { PNN_FP32 = 0, PNN_BF16 = 1 };
 /* Training kernel selection (pnn_set_kernel). */
 enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          */
        PNN_KERNEL_REFERENCE = 1, /* one CTA per CN, weights in global memory    */
-       PNN_KERNEL_RESIDENT = 2,  /* persistent cluster kernel, on-chip weights:
-                                    W1 in registers (2-layer nets, 768 < D <=
-                                    784, O = 10, H <= 256).  Variant v8 (chain
-                                    on rotating warp pairs, 2 SMs per CN at
-                                    H = 128) or v10 (chain on its own CTA, one
-                                    SM more, shorter period): AUTO takes v10
-                                    when all concurrently trained CNs fit the
-                                    GPU (K_local or slots x 3 <= 148, H <= 128);
-                                    environment PNN_RESIDENT_V10=0/1 forces.   */
+       PNN_KERNEL_RESIDENT = 2,  /* persistent per-CN kernel, on-chip weights
+                                    (2-layer nets, 768 < D <= 784, O = 10,
+                                    H <= 256); variants (pnn_set_variant):
+                                    TMEM (one SM per CN, W1 in registers +
+                                    tensor memory, H <= 128), v8 (W1 in the
+                                    registers of a cluster, chain on rotating
+                                    warp pairs) and v10 (chain on its own CTA).
+                                    AUTO: v10 when every concurrently trained
+                                    CN fits with its chain CTA (K_local or
+                                    slots x 3 <= 120, H <= 128), else TMEM
+                                    (H <= 128), else v8.                       */
        PNN_KERNEL_TC_BF16 = 3,   /* bf16 mini-batch on tcgen05 GEMMs; chosen by
                                     pnn_set_minibatch(.., PNN_BF16), reported
                                     by pnn_kernel_info, not settable         */
@@ -110,8 +112,23 @@ enum { PNN_KERNEL_AUTO = 0,      /* fastest kernel valid for the shape          
                                     3-layer nets with 768 < D <= 784, H1 <= 320,
                                     H2 <= 120, O <= 16 run its deep variant
                                     (W1 in registers, k_deep.cu; 2 launches per
-                                    epoch in pnn_kernel_info); environment
-                                    PNN_DEEP=0 selects the generic kernel.    */ };
+                                    epoch in pnn_kernel_info);
+                                    PNN_VARIANT_CLUSTER_GENERIC forces the
+                                    generic kernel.                           */ };
+
+/* Kernel variant inside a family (pnn_set_variant / pnn_kernel_variant).  All
+ * variants of a family compute the same method (§3); they differ in
+ * data placement and schedule, so results agree to rounding (DESIGN.md §3 R27). */
+enum { PNN_VARIANT_AUTO = 0,             /* the family's AUTO rule              */
+       PNN_VARIANT_RESIDENT_V8 = 8,      /* W1 in the registers of a 1-4 CTA
+                                            cluster, chain on warp pairs        */
+       PNN_VARIANT_RESIDENT_V10 = 10,    /* sweep CTA(s) + a dedicated chain CTA */
+       PNN_VARIANT_RESIDENT_TMEM = 11,   /* one SM per CN: W1 in registers and
+                                            tensor memory (H <= 128)            */
+       PNN_VARIANT_CLUSTER_GENERIC = 20, /* any depth, weights in shared memory  */
+       PNN_VARIANT_CLUSTER_DEEP = 21,    /* 3-layer nets, W1 in registers       */
+       PNN_VARIANT_MB_STEP = 30,         /* fp32 mini-batch: step kernels       */
+       PNN_VARIANT_MB_RESIDENT = 31 };   /* fp32 mini-batch: one launch/epoch   */
 
 /* Build a PNN of n_subnets CNs with layer sizes layers[0..n_layers-1]
  * (layers[0] = inputs, e.g. {784,128,10}; n_layers >= 2, each size >= 1,
@@ -156,6 +173,20 @@ pnn_status pnn_set_minibatch(pnn_net net, int32_t batch, int32_t precision);
  * not fit them; _TC_BF16 and _MB_F32 are not settable.    */
 pnn_status pnn_set_kernel(pnn_net net, int32_t kernel);
 
+/* Force a kernel variant (PNN_VARIANT_*; AUTO restores the rule).  A non-AUTO
+ * variant also selects its family (as pnn_set_kernel would); pnn_set_kernel
+ * resets the variant to AUTO.  The variant must support the shape and the
+ * current mini-batch setting (pnn_set_minibatch first).  The choice is fixed
+ * here, not read from the environment, and pnn_kernel_variant reports it.
+ * Errors: PNN_ERR_INVALID (unknown variant, or the shape / batch does not fit
+ * it: the message says why).                                                 */
+pnn_status pnn_set_variant(pnn_net net, int32_t variant);
+
+/* The variant (PNN_VARIANT_*) the next pnn_train_epoch launches: the forced one or
+ * AUTO's resolution; PNN_VARIANT_AUTO for kernels without variants (reference,
+ * bf16).  Errors: PNN_ERR_INVALID.                                             */
+pnn_status pnn_kernel_variant(pnn_net net, int32_t* variant);
+
 /* Limit how many local CNs train concurrently (the GPU
  * analogue of the paper's goroutine count, Table 2): each
  * pnn_train_epoch then trains the CNs in consecutive waves of `slots` CNs, one
@@ -165,7 +196,9 @@ pnn_status pnn_set_kernel(pnn_net net, int32_t kernel);
 pnn_status pnn_set_slots(pnn_net net, int32_t slots);
 
 /* One training epoch of every local CN ("Each child-network
- * learns only a slice of the dataset"; :225-231).  x: device fp32
+ * learns only a slice of the dataset"; :225-231).  On a rank that owns no CN
+ * (K < nranks) the call is a no-op that needs n = 0 (x / labels may be NULL).
+ * x: device fp32
  * [n][layers[0]] row-major; labels: device int32 [n], each in
  * [0, layers[n_layers-1]) (the one-hot target e of Eqs.6-10 is implicit).
  * n = this rank's rows: the concatenated slices of its CNs, split among them
@@ -191,6 +224,18 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* x_host, const int32_t*
  * rounding to fp32.  CNs are left untouched.  Asynchronous.
  * Errors: PNN_ERR_STATE, PNN_ERR_CUDA, PNN_ERR_NCCL.                         */
 pnn_status pnn_merge(pnn_net net, void* cuda_stream);
+
+/* The two device steps of pnn_merge around its all-reduce, for callers that run
+ * the cross-rank reduction themselves (e.g. torch.distributed) and for testing
+ * the multi-rank arithmetic on one GPU.  pnn_merge_partial: sum_out (device fp64
+ * [P_total], caller-owned) = Σ of this rank's CNs in ascending CN order (zeros on a
+ * rank that owns no CN).  pnn_merge_finish: merged := (float)(sum / K) from a
+ * device fp64 [P_total] that holds the sum over ALL K CNs (PAPER.md:233-238,
+ * R18).  pnn_merge with nranks > 1 is exactly partial → ncclAllReduce(sum, fp64)
+ * → finish.  Asynchronous.  Errors: PNN_ERR_INVALID (NULL pointer),
+ * PNN_ERR_STATE, PNN_ERR_CUDA.                                               */
+pnn_status pnn_merge_partial(pnn_net net, double* sum_out, void* cuda_stream);
+pnn_status pnn_merge_finish(pnn_net net, const double* sum, void* cuda_stream);
 
 /* Classify n rows of x (device fp32 [n][layers[0]]) with the merged network
  * (subnet = -1) or local CN `subnet` (global index): labels_out[i] (device
@@ -238,6 +283,13 @@ int64_t pnn_param_count(pnn_net net);
 
 /* This rank's CN range [*first, *first + *count).  Errors: PNN_ERR_INVALID. */
 pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count);
+
+/* The rows of an n_total-row training set this rank trains on (PAPER.md:166-169
+ * slicing, R17 over all K CNs): [*first, *first + *count) = the concatenated
+ * slices of its CNs, which is what pnn_train_epoch expects as x / labels.  A rank
+ * that owns no CN (K < nranks) gets *count = 0.  Errors: PNN_ERR_INVALID (NULL
+ * pointer, n_total < K).                                                      */
+pnn_status pnn_local_rows(pnn_net net, int64_t n_total, int64_t* first, int64_t* count);
 
 /* Which training kernel the next pnn_train_epoch launches (PNN_KERNEL_*),
  * and how many kernel launches it makes (PNN_KERNEL_TC_BF16: launches per

@@ -618,8 +618,6 @@ int deep_cluster(const NetDesc& d) {
 }  // namespace
 
 const char* deep_plan(const NetDesc& d, int batch) {
-    const char* v = getenv("PNN_DEEP");
-    if (v && v[0] == '0') return "disabled (PNN_DEEP=0)";
     if (batch != 1) return "per-sample SGD only";
     if (d.L != 3) return "3-layer nets only";
     const int D = d.n[0];

@@ -485,8 +485,6 @@ cudaError_t launch_c(const NetDesc& d, float* children, const float* x, const in
 }  // namespace
 
 const char* mbres_plan(const NetDesc& d, int batch) {
-    const char* v = getenv("PNN_MBRES");
-    if (v && v[0] == '0') return "disabled (PNN_MBRES=0)";
     if (d.L != 2) return "2-layer nets only";
     if (batch < 2 || batch > BMX) return "batches of 2..64";
     const int D = d.n[0];

@@ -1666,13 +1666,16 @@ cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long 
     return cudaGetLastError();
 }
 
-ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent) {
+ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int variant) {
     ResidentPlan p{};
     auto no = [&](const char* why) {
         p.ok = false;
         snprintf(p.why, sizeof p.why, "%s", why);
         return p;
     };
+    if (variant != PNN_VARIANT_AUTO && variant != PNN_VARIANT_RESIDENT_V8 && variant != PNN_VARIANT_RESIDENT_V10 &&
+        variant != PNN_VARIANT_RESIDENT_TMEM)
+        return no("not a resident-kernel variant");
     if (batch != 1) return no("mini-batch runs on the reference kernel");
     if (d.L != 2) return no("resident kernel covers 2-layer nets (D-H-O)");
     const int D = d.n[0], H = d.n[1], Od = d.n[2];
@@ -1689,24 +1692,38 @@ ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent) {
     int c = 1;
     while (c <= CMAX && (H + c - 1) / c > UMAX) c *= 2;
     if (c > CMAX) return no("hidden layer wider than 256");
-    p.cluster = c;
-    p.groups = 1;
-    p.threads = NW * 32;                           // 8 warps; rows >= U are idle
-    p.smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
-    p.variant = 8;
+    // v11 (k_tmem.cu): one SM per CN, W1 in registers + tensor memory, no cross-SM exchange
+    // and no Gram pre-pass; H <= 128.
+    const bool tm_ok = tmem_plan(d, batch) == nullptr;
     // v10 (the chain on its own CTA) for H <= 128: 1 or 2 sweep CTAs + 1 chain CTA.  It costs one
     // SM more per CN but shortens the per-sample period: measured faster when every CN runs at
-    // once (C2 +11 %, C1 +5 %), slower when the SMs are the limit (C4: 43.6 vs 64.4 M samples/s;
-    // DESIGN.md §5).  AUTO takes it when `concurrent` CNs × its cluster fit the 148 SMs;
-    // PNN_RESIDENT_V10=1 / =0 force it on / off.
-    const char* v10 = getenv("PNN_RESIDENT_V10");
+    // once (C2 +11 %, C1 +5 %), slower when the SMs are the limit.  AUTO takes it
+    // when `concurrent` CNs × its cluster fit (≤ 120 SMs: 3-CTA clusters do not all fit 148 SMs
+    // at once; K = 48 measured slower than v8).
     const int c10 = (H + UMAX - 1) / UMAX + 1;
-    // (≤ 120 SMs: 3-CTA clusters do not all fit 148 SMs at once; K = 48 measured slower than v8)
-    const bool want10 = v10 && v10[0] ? v10[0] == '1' : (concurrent > 0 && (long long)concurrent * c10 <= 120);
-    if (H <= 2 * UMAX && want10) {
+    const bool v10_ok = H <= 2 * UMAX;
+    int v = variant;
+    if (v == PNN_VARIANT_AUTO) {
+        if (v10_ok && concurrent > 0 && (long long)concurrent * c10 <= 120) v = PNN_VARIANT_RESIDENT_V10;
+        else if (tm_ok) v = PNN_VARIANT_RESIDENT_TMEM;
+        else v = PNN_VARIANT_RESIDENT_V8;
+    }
+    if (v == PNN_VARIANT_RESIDENT_TMEM && !tm_ok) return no("TMEM variant: hidden layer wider than 128");
+    if (v == PNN_VARIANT_RESIDENT_V10 && !v10_ok) return no("v10 variant: hidden layer wider than 128");
+    p.groups = 1;
+    p.threads = NW * 32;                           // 8 warps; rows >= U are idle
+    if (v == PNN_VARIANT_RESIDENT_V8) {
+        p.variant = 8;
+        p.cluster = c;
+        p.smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
+    } else if (v == PNN_VARIANT_RESIDENT_V10) {
         p.variant = 10;
-        p.cluster = (H + UMAX - 1) / UMAX + 1;
+        p.cluster = c10;
         p.smem = kSplitHead + sizeof(float) * (size_t)(S + 1) * DP;   // + the zero row (paired sweeps)
+    } else {
+        p.variant = 11;
+        p.cluster = 1;
+        p.smem = 0;                                // sized by launch_sgd_tmem
     }
     p.ok = true;
     return p;
@@ -1721,8 +1738,15 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 int K_local, int s_first, int s_count, float lr, cudaStream_t st,
                                 cudaEvent_t ev0, cudaEvent_t ev1) {
     if (s_count <= 0) return cudaSuccess;
+    cudaError_t e;
+    if (p.variant == 11) {                         // v11 forms its Gram terms in the launch
+        if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
+        e = launch_sgd_tmem(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st);
+        if (e != cudaSuccess || !ev1) return e;
+        return cudaEventRecord(ev1, st);
+    }
     gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (ev0) {                                     // timing hook: bracket the SGD launch only
         if ((e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;

@@ -26,6 +26,7 @@ struct pnn_net_s {
     int k_first = 0, K_local = 1;     // this rank's CNs [k_first, k_first + K_local)
     void* comm = nullptr;             // ncclComm_t
     int batch = 1, precision = PNN_FP32, kernel = PNN_KERNEL_AUTO;
+    int variant = PNN_VARIANT_AUTO;   // forced kernel variant (pnn_set_variant)
     int slots = 0;                    // CNs trained concurrently (0 = all local CNs; f4)
     bool timing = false;              // record CUDA events around each training-kernel launch
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -161,19 +162,52 @@ pnn_status alloc_local(pnn_net net) {
     return PNN_OK;
 }
 
-int choose_kernel(pnn_net net, ResidentPlan* plan) {
+bool is_resident_variant(int v) {
+    return v == PNN_VARIANT_RESIDENT_V8 || v == PNN_VARIANT_RESIDENT_V10 || v == PNN_VARIANT_RESIDENT_TMEM;
+}
+
+// The kernel family (PNN_KERNEL_*, -1 when a forced choice does not fit) and, in *var, the
+// variant the next epoch launches.  Everything comes from the handle: no environment reads.
+int choose_kernel(pnn_net net, ResidentPlan* plan, int* var = nullptr) {
+    int vdummy = 0;
+    int& v = var ? *var : vdummy;
+    v = PNN_VARIANT_AUTO;
+    const int fv = net->variant;
     if (net->precision == PNN_BF16) return PNN_KERNEL_TC_BF16;
-    if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1 && !mbres_plan(net->d, net->batch))
-        return PNN_KERNEL_MB_RESIDENT;
-    if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1 && !mb32_plan(net->d, net->batch))
-        return PNN_KERNEL_MB_F32;
+    if (fv == PNN_VARIANT_MB_STEP || fv == PNN_VARIANT_MB_RESIDENT) {
+        if (net->batch < 2) return -1;
+        if (fv == PNN_VARIANT_MB_RESIDENT && mbres_plan(net->d, net->batch)) return -1;
+        if (fv == PNN_VARIANT_MB_STEP && mb32_plan(net->d, net->batch)) return -1;
+    }
+    if (net->kernel != PNN_KERNEL_REFERENCE && net->batch > 1) {
+        if (fv != PNN_VARIANT_MB_STEP && !mbres_plan(net->d, net->batch)) {
+            v = PNN_VARIANT_MB_RESIDENT;
+            return PNN_KERNEL_MB_RESIDENT;
+        }
+        if (!mb32_plan(net->d, net->batch)) {
+            v = PNN_VARIANT_MB_STEP;
+            return PNN_KERNEL_MB_F32;
+        }
+    }
     if (net->kernel == PNN_KERNEL_REFERENCE) return PNN_KERNEL_REFERENCE;
-    if (net->kernel == PNN_KERNEL_CLUSTER) return plan_cluster(net->d, net->batch).ok ? PNN_KERNEL_CLUSTER : -1;
+    auto cluster = [&]() -> int {
+        if (!plan_cluster(net->d, net->batch).ok) return -1;
+        const bool deep_ok = deep_plan(net->d, net->batch) == nullptr;
+        if (fv == PNN_VARIANT_CLUSTER_DEEP && !deep_ok) return -1;
+        v = (deep_ok && fv != PNN_VARIANT_CLUSTER_GENERIC) ? PNN_VARIANT_CLUSTER_DEEP : PNN_VARIANT_CLUSTER_GENERIC;
+        return PNN_KERNEL_CLUSTER;
+    };
+    if (net->kernel == PNN_KERNEL_CLUSTER) return cluster();
     const int conc = (net->slots > 0 && net->slots < net->K_local) ? net->slots : net->K_local;
-    *plan = plan_resident(net->d, net->batch, conc);
+    *plan = plan_resident(net->d, net->batch, conc, is_resident_variant(fv) ? fv : PNN_VARIANT_AUTO);
+    if (plan->ok)
+        v = plan->variant == 8 ? PNN_VARIANT_RESIDENT_V8
+            : plan->variant == 10 ? PNN_VARIANT_RESIDENT_V10 : PNN_VARIANT_RESIDENT_TMEM;
     if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
     if (plan->ok) return PNN_KERNEL_RESIDENT;
-    return plan_cluster(net->d, net->batch).ok ? PNN_KERNEL_CLUSTER : PNN_KERNEL_REFERENCE;
+    v = PNN_VARIANT_AUTO;
+    const int c = cluster();
+    return c >= 0 ? c : PNN_KERNEL_REFERENCE;
 }
 
 pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long long n,
@@ -195,8 +229,9 @@ pnn_status launch_train(pnn_net net, const float* x, const int32_t* y, long long
 pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long long n,
                              int s_first, int s_count, cudaStream_t st) {
     ResidentPlan plan{};
-    int k = choose_kernel(net, &plan);
-    if (k < 0) return fail(net, PNN_ERR_INVALID, "forced kernel not valid here: %s", plan.why);
+    int var = PNN_VARIANT_AUTO;
+    int k = choose_kernel(net, &plan, &var);
+    if (k < 0) return fail(net, PNN_ERR_INVALID, "forced kernel / variant not valid here: %s", plan.why);
     cudaError_t e;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (net->timing && s_count > 0) {
@@ -205,8 +240,9 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         net->tev.emplace_back(ev0, ev1);
         if (k != PNN_KERNEL_RESIDENT) CUDA_TRY(net, cudaEventRecord(ev0, st));   // the resident path
     }                                                                               // brackets its SGD launch
-    const bool deep = k == PNN_KERNEL_CLUSTER && !deep_plan(net->d, net->batch);
-    if ((k == PNN_KERNEL_RESIDENT || deep) && net->gram_rows < n) {   // 32-B Gram records (R27)
+    const bool deep = var == PNN_VARIANT_CLUSTER_DEEP;
+    const bool gram = deep || (k == PNN_KERNEL_RESIDENT && var != PNN_VARIANT_RESIDENT_TMEM);
+    if (gram && net->gram_rows < n) {                                // 32-B Gram records (R27)
         cudaFree(net->d_gram);
         net->d_gram = nullptr;
         net->gram_rows = 0;
@@ -255,6 +291,8 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
 }
 
 pnn_status check_rows(pnn_net net, long long n) {
+    if (net->K_local <= 0)
+        return n == 0 ? PNN_OK : fail(net, PNN_ERR_DATA, "this rank owns no CN: n must be 0 (got %lld)", n);
     if (n < net->K_local)
         return fail(net, PNN_ERR_DATA, "n = %lld rows < %d local CNs: some CN would get an empty slice",
                     n, net->K_local);
@@ -396,6 +434,57 @@ pnn_status pnn_set_kernel(pnn_net net, int32_t kernel) {
         if (!p.ok) return fail(net, PNN_ERR_INVALID, "resident kernel not valid: %s", p.why);
     }
     net->kernel = kernel;
+    net->variant = PNN_VARIANT_AUTO;
+    return PNN_OK;
+}
+
+pnn_status pnn_set_variant(pnn_net net, int32_t variant) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    switch (variant) {
+    case PNN_VARIANT_AUTO:
+        break;
+    case PNN_VARIANT_RESIDENT_V8:
+    case PNN_VARIANT_RESIDENT_V10:
+    case PNN_VARIANT_RESIDENT_TMEM: {
+        ResidentPlan p = plan_resident(net->d, net->batch, 0, variant);
+        if (!p.ok) return fail(net, PNN_ERR_INVALID, "variant %d not valid: %s", variant, p.why);
+        net->kernel = PNN_KERNEL_RESIDENT;
+        break;
+    }
+    case PNN_VARIANT_CLUSTER_GENERIC:
+    case PNN_VARIANT_CLUSTER_DEEP: {
+        ClusterPlan p = plan_cluster(net->d, net->batch);
+        if (!p.ok) return fail(net, PNN_ERR_INVALID, "variant %d not valid: %s", variant, p.why);
+        if (variant == PNN_VARIANT_CLUSTER_DEEP)
+            if (const char* why = deep_plan(net->d, net->batch))
+                return fail(net, PNN_ERR_INVALID, "variant %d not valid: %s", variant, why);
+        net->kernel = PNN_KERNEL_CLUSTER;
+        break;
+    }
+    case PNN_VARIANT_MB_STEP:
+    case PNN_VARIANT_MB_RESIDENT: {
+        if (net->precision != PNN_FP32 || net->batch < 2)
+            return fail(net, PNN_ERR_INVALID, "variant %d needs an fp32 mini-batch (pnn_set_minibatch first)",
+                        variant);
+        const char* why = variant == PNN_VARIANT_MB_STEP ? mb32_plan(net->d, net->batch) : mbres_plan(net->d, net->batch);
+        if (why) return fail(net, PNN_ERR_INVALID, "variant %d not valid: %s", variant, why);
+        net->kernel = PNN_KERNEL_AUTO;
+        break;
+    }
+    default:
+        return fail(net, PNN_ERR_INVALID, "variant = %d unknown", variant);
+    }
+    net->variant = variant;
+    return PNN_OK;
+}
+
+pnn_status pnn_kernel_variant(pnn_net net, int32_t* variant) {
+    if (!net || !variant) return PNN_ERR_INVALID;
+    ResidentPlan plan{};
+    int v = PNN_VARIANT_AUTO;
+    choose_kernel(net, &plan, &v);
+    *variant = v;
     return PNN_OK;
 }
 
@@ -433,6 +522,7 @@ pnn_status pnn_train_epoch(pnn_net net, const float* x, const int32_t* labels, i
                            void* stream) {
     pnn_status st = check_live(net);
     if (st) return st;
+    if (net->K_local == 0) return check_rows(net, n);   // idle rank (K < nranks)
     if (!x || !labels) return fail(net, PNN_ERR_INVALID, "x/labels is NULL");
     if ((st = check_rows(net, n))) return st;
     CUDA_TRY(net, cudaSetDevice(net->device));
@@ -443,6 +533,7 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
                                 void* stream) {
     pnn_status st = check_live(net);
     if (st) return st;
+    if (net->K_local == 0) return check_rows(net, n);   // idle rank (K < nranks)
     if (!xh || !yh) return fail(net, PNN_ERR_INVALID, "x/labels is NULL");
     if ((st = check_rows(net, n))) return st;
     CUDA_TRY(net, cudaSetDevice(net->device));
@@ -461,12 +552,13 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
     int groups = 1;
     {
         ResidentPlan rp{};
-        const int k = choose_kernel(net, &rp);
+        int var = PNN_VARIANT_AUTO;
+        const int k = choose_kernel(net, &rp, &var);
         int cap = net->K_local;                   // CNs that run concurrently
         if (k == PNN_KERNEL_RESIDENT) cap = 148 / (rp.cluster > 0 ? rp.cluster : 1);
         else if (k == PNN_KERNEL_CLUSTER)
-            cap = 148 / (deep_plan(net->d, net->batch) ? plan_cluster(net->d, net->batch).cluster
-                                                       : deep_cluster_size(net->d));
+            cap = 148 / (var == PNN_VARIANT_CLUSTER_DEEP ? deep_cluster_size(net->d)
+                                                         : plan_cluster(net->d, net->batch).cluster);
         else if (k == PNN_KERNEL_REFERENCE) cap = 148;
         else if (k == PNN_KERNEL_MB_RESIDENT) cap = 148 / mbres_cluster(net->d);
         groups = net->K_local / (cap > 0 ? cap : 1);
@@ -516,6 +608,24 @@ pnn_status pnn_merge(pnn_net net, void* stream) {
                                       (ncclComm_t)net->comm, cs);
     if (r != ncclSuccess) return fail(net, PNN_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
     CUDA_TRY(net, launch_merge_finish(net->d_msum, P, net->K, net->d_merged, cs));
+    return PNN_OK;
+}
+
+pnn_status pnn_merge_partial(pnn_net net, double* sum_out, void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!sum_out) return fail(net, PNN_ERR_INVALID, "sum_out is NULL");
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    CUDA_TRY(net, launch_merge_sum(net->d_children, net->K_local, net->d.P, sum_out, (cudaStream_t)stream));
+    return PNN_OK;
+}
+
+pnn_status pnn_merge_finish(pnn_net net, const double* sum, void* stream) {
+    pnn_status st = check_live(net);
+    if (st) return st;
+    if (!sum) return fail(net, PNN_ERR_INVALID, "sum is NULL");
+    CUDA_TRY(net, cudaSetDevice(net->device));
+    CUDA_TRY(net, launch_merge_finish(sum, net->d.P, net->K, net->d_merged, (cudaStream_t)stream));
     return PNN_OK;
 }
 
@@ -613,16 +723,36 @@ pnn_status pnn_local_subnets(pnn_net net, int32_t* first, int32_t* count) {
     return PNN_OK;
 }
 
+pnn_status pnn_local_rows(pnn_net net, int64_t n_total, int64_t* first, int64_t* count) {
+    if (!net || !first || !count) return PNN_ERR_INVALID;
+    if (n_total < net->K)
+        return fail(net, PNN_ERR_INVALID, "n_total = %lld < K = %d", (long long)n_total, net->K);
+    if (net->K_local == 0) {
+        long long s0 = n_total, c0 = 0;
+        if (net->k_first < net->K) shard_of(n_total, net->K, net->k_first, &s0, &c0);
+        *first = s0;
+        *count = 0;
+        return PNN_OK;
+    }
+    long long s0, c0, s1, c1;
+    shard_of(n_total, net->K, net->k_first, &s0, &c0);
+    shard_of(n_total, net->K, net->k_first + net->K_local - 1, &s1, &c1);
+    *first = s0;
+    *count = s1 + c1 - s0;
+    return PNN_OK;
+}
+
 pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     if (!net || !kernel || !launches) return PNN_ERR_INVALID;
     ResidentPlan plan{};
-    int k = choose_kernel(net, &plan);
+    int v = PNN_VARIANT_AUTO;
+    int k = choose_kernel(net, &plan, &v);
     *kernel = k < 0 ? PNN_KERNEL_REFERENCE : k;
-    // resident: Gram terms + training; tc bf16: weight cast + 7 per mini-batch step
-    // deep cluster variant (3 layers): Gram terms + training
-    const bool deep = k == PNN_KERNEL_CLUSTER && !deep_plan(net->d, net->batch);
-    *launches = (k == PNN_KERNEL_RESIDENT || deep) ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
-    // (PNN_KERNEL_MB_RESIDENT: 1 per epoch)
+    // resident v8 / v10 and the deep cluster variant: Gram terms + training; the TMEM variant
+    // forms its Gram terms in the training launch; tc bf16: 7 per mini-batch step; fp32 step
+    // kernels: 4 per step; MB_RESIDENT: 1 per epoch
+    const bool gram = v == PNN_VARIANT_CLUSTER_DEEP || (k == PNN_KERNEL_RESIDENT && v != PNN_VARIANT_RESIDENT_TMEM);
+    *launches = gram ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
     return PNN_OK;
 }
 

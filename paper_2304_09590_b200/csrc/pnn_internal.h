@@ -50,14 +50,21 @@ struct ResidentPlan {
     int variant;        // template instance id
     char why[160];      // reason when !ok
 };
-// concurrent: CNs trained at once (0 = unknown: v8); see plan_resident's v10 rule
-ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent = 0);
+// concurrent: CNs trained at once (0 = unknown); variant: PNN_VARIANT_AUTO or a forced
+// PNN_VARIANT_RESIDENT_* (see plan_resident's rule)
+ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent = 0, int variant = 0);
 // gram: scratch of 2·n_local float4 (32-B records: the lookahead's Gram terms and the
 // label of every row, recomputed per call).
 cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* children,
                                 const float* x, const int32_t* labels, float4* gram, long long n_local,
                                 int K_local, int s_first, int s_count, float lr,
                                 cudaStream_t st, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+
+// TMEM variant (k_tmem.cu, v11): one SM per CN, W¹ rows in registers + tensor memory,
+// Gram terms formed in the launch.  nullptr when the shape is supported.
+const char* tmem_plan(const NetDesc& d, int batch);
+cudaError_t launch_sgd_tmem(const NetDesc& d, float* children, const float* x, const int32_t* y, long long n_local,
+                            int K_local, int s_first, int s_count, float lr, cudaStream_t st);
 
 // The lookahead's Gram records (32 B per row: x(u-4..u-1)·x(u) and the label), k_resident.cu.
 cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,

@@ -24,6 +24,11 @@ PNN_INIT_NORMAL, PNN_INIT_UNIFORM, PNN_INIT_XAVIER_NORMAL, PNN_INIT_HE_NORMAL = 
 PNN_FP32, PNN_BF16 = 0, 1
 PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16, PNN_KERNEL_MB_F32, \
     PNN_KERNEL_CLUSTER, PNN_KERNEL_MB_RESIDENT = 0, 1, 2, 3, 4, 5, 6
+PNN_VARIANT_AUTO, PNN_VARIANT_RESIDENT_V8, PNN_VARIANT_RESIDENT_V10, PNN_VARIANT_RESIDENT_TMEM = 0, 8, 10, 11
+PNN_VARIANT_CLUSTER_GENERIC, PNN_VARIANT_CLUSTER_DEEP, PNN_VARIANT_MB_STEP, PNN_VARIANT_MB_RESIDENT = 20, 21, 30, 31
+VARIANT = {"auto": PNN_VARIANT_AUTO, "v8": PNN_VARIANT_RESIDENT_V8, "v10": PNN_VARIANT_RESIDENT_V10,
+           "tmem": PNN_VARIANT_RESIDENT_TMEM, "cluster": PNN_VARIANT_CLUSTER_GENERIC, "deep": PNN_VARIANT_CLUSTER_DEEP,
+           "mb_step": PNN_VARIANT_MB_STEP, "mb_resident": PNN_VARIANT_MB_RESIDENT}
 ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX,
        "leaky_relu": PNN_LEAKY_RELU}
 INIT = {"normal": PNN_INIT_NORMAL, "uniform": PNN_INIT_UNIFORM, "xavier": PNN_INIT_XAVIER_NORMAL,
@@ -34,7 +39,8 @@ KERNEL = {"auto": PNN_KERNEL_AUTO, "reference": PNN_KERNEL_REFERENCE, "resident"
 EXPORTS = ["pnn_create", "pnn_set_comm", "pnn_set_minibatch", "pnn_set_kernel", "pnn_train_epoch",
            "pnn_train_epoch_host", "pnn_merge", "pnn_predict", "pnn_get_params", "pnn_set_params",
            "pnn_device_params", "pnn_param_count", "pnn_local_subnets", "pnn_kernel_info",
-           "pnn_last_error", "pnn_destroy", "pnn_evaluate", "pnn_set_slots", "pnn_kernel_timing"]
+           "pnn_last_error", "pnn_destroy", "pnn_evaluate", "pnn_set_slots", "pnn_kernel_timing",
+           "pnn_set_variant", "pnn_kernel_variant", "pnn_local_rows", "pnn_merge_partial", "pnn_merge_finish"]
 
 _lib = None
 
@@ -78,6 +84,11 @@ def load(path: str | None = None):
         "pnn_evaluate": ([V, I32, V, V, I64, V, V], I32),
         "pnn_set_slots": ([V, I32], I32),
         "pnn_kernel_timing": ([V, I32, V, V], I32),
+        "pnn_set_variant": ([V, I32], I32),
+        "pnn_kernel_variant": ([V, P32], I32),
+        "pnn_local_rows": ([V, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)], I32),
+        "pnn_merge_partial": ([V, V, V], I32),
+        "pnn_merge_finish": ([V, V, V], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -150,8 +161,32 @@ class PNN:
     def set_kernel(self, kernel):
         self._check(self._L.pnn_set_kernel(self.h, KERNEL[kernel] if isinstance(kernel, str) else kernel))
 
+    def set_variant(self, variant):
+        self._check(self._L.pnn_set_variant(self.h, VARIANT[variant] if isinstance(variant, str) else variant))
+
+    def kernel_variant(self) -> int:
+        v = ctypes.c_int32()
+        self._check(self._L.pnn_kernel_variant(self.h, ctypes.byref(v)))
+        return v.value
+
+    def local_rows(self, n_total):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._L.pnn_local_rows(self.h, int(n_total), ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def merge_partial(self, sum_out, stream=None):
+        import torch
+        self._check(self._L.pnn_merge_partial(self.h, _ptr(sum_out, torch.float64), ctypes.c_void_p(_stream_ptr(stream))))
+
+    def merge_finish(self, total, stream=None):
+        import torch
+        self._check(self._L.pnn_merge_finish(self.h, _ptr(total, torch.float64), ctypes.c_void_p(_stream_ptr(stream))))
+
     def train_epoch(self, x, labels, stream=None):
         import torch
+        if x is None or x.shape[0] == 0:       # an idle rank (owns no CN): n = 0, NULL pointers
+            self._check(self._L.pnn_train_epoch(self.h, None, None, 0, ctypes.c_void_p(_stream_ptr(stream))))
+            return
         assert x.dim() == 2 and x.shape[1] == self.layers[0] and labels.shape == (x.shape[0],)
         self._check(self._L.pnn_train_epoch(self.h, _ptr(x, torch.float32), _ptr(labels, torch.int32),
                                             x.shape[0], ctypes.c_void_p(_stream_ptr(stream))))

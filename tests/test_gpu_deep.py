@@ -3,7 +3,7 @@ registers of a cluster of 4 or 8 CTAs, R27 lookahead) against the fp32 oracle.
 
 The variant is what the cluster kernel (and AUTO) runs for 3-layer shapes with
 768 < D <= 784, H1 <= 320, O <= 16 and per-sample SGD (C3: 784-300-100-10);
-PNN_DEEP=0 falls back to the generic cluster kernel.  Tolerance as everywhere for
+the PNN_VARIANT_CLUSTER_GENERIC variant selects the generic cluster kernel.  Tolerance as everywhere for
 fp32 per-sample SGD: max-abs 1e-4 on every parameter (BASELINE.json north_star).
 """
 import numpy as np
@@ -31,12 +31,14 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def _run(orc, layers, act, init, K, lr, n, epochs=1, kernel="auto", deep=True):
+def _run(orc, layers, act, init, K, lr, n, epochs=1, kernel="auto", variant=None):
     from paper_2304_09590_b200 import PNN
     X, y = make_split(n, "train", 0)
     X = np.ascontiguousarray(X[:, :layers[0]])
     net = PNN(layers, act, init, K, lr, seed=0)
     net.set_kernel(kernel)
+    if variant is not None:
+        net.set_variant(variant)
     kinfo = net.kernel_info()
     xd, yd = dev(X), dev(y)
     for _ in range(epochs):
@@ -83,9 +85,8 @@ def test_short_slices(orc, rows_per_cn):
     _run(orc, c.layers, c.act, c.init, K, 0.05, n, epochs=2)
 
 
-def test_generic_cluster_fallback(orc, monkeypatch):
-    """PNN_DEEP=0: the generic cluster kernel (weights in shared memory) on the C3 shape."""
-    monkeypatch.setenv("PNN_DEEP", "0")
+def test_generic_cluster_fallback(orc):
+    """The generic cluster kernel (weights in shared memory) on the C3 shape."""
     c = CONFIGS["C3"]
-    kinfo = _run(orc, c.layers, c.act, c.init, 4, c.lr, 4 * 100 + 3, kernel="cluster")
+    kinfo = _run(orc, c.layers, c.act, c.init, 4, c.lr, 4 * 100 + 3, kernel="cluster", variant="cluster")
     assert tuple(kinfo) == (5, 1)

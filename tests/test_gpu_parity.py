@@ -44,10 +44,12 @@ def dev(a):
 KERNELS = ["reference", "auto"]
 
 
-def _train(cfg_layers, act, init, K, lr, X, y, epochs=1, kernel="auto", batch=1):
+def _train(cfg_layers, act, init, K, lr, X, y, epochs=1, kernel="auto", batch=1, variant=None):
     net = PNN(cfg_layers, act, init, K, lr, seed=0, kernel=kernel)
     if batch > 1:
         net.set_minibatch(batch)
+    if variant is not None:
+        net.set_variant(variant)
     xd, yd = dev(X), dev(y)
     for _ in range(epochs):
         net.train_epoch(xd, yd)
@@ -184,36 +186,62 @@ def test_cluster_kernel(orc, name, K, n, epochs):
     assert np.abs(merged - omerged).max() < TOL
 
 
-@pytest.mark.parametrize("kernel", ["resident", "resident_v8", "cluster", "reference"])
+@pytest.mark.parametrize("kernel", ["resident", "v8", "tmem", "cluster", "reference"])
 @pytest.mark.parametrize("rows_per_cn", [1, 2, 3, 4, 5, 6, 17])
-def test_short_slices(orc, kernel, rows_per_cn, monkeypatch):
-    """Slices shorter than the resident kernel's lookahead / prefetch depths (L = 4,
+def test_short_slices(orc, kernel, rows_per_cn):
+    """Slices shorter than the resident kernels' lookahead / prefetch depths (L = 4,
     8 rows in flight) and the cluster kernel's ring, with one ragged slice.  6 CNs fit
-    the GPU, so AUTO's resident plan is v10; resident_v8 forces v8 (PNN_RESIDENT_V10=0)."""
-    if kernel == "resident_v8":
-        monkeypatch.setenv("PNN_RESIDENT_V10", "0")
-        kernel = "resident"
+    the GPU, so AUTO's resident plan is v10; v8 / tmem force those variants."""
+    variant = None
+    if kernel in ("v8", "tmem"):
+        variant, kernel = kernel, "resident"
     c = CONFIGS["C4"]
     K = 6
     n = K * rows_per_cn + (1 if rows_per_cn > 1 else 0)
     X, y = make_split(n, "train", 0)
-    _, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, 2, kernel)
+    _, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, 2, kernel, variant=variant)
     okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=2)
     assert np.abs(kids - okids).max() < TOL
     assert np.abs(merged - omerged).max() < TOL
 
 
-def test_resident_v10_split_variant(orc, monkeypatch):
-    """The opt-in v10 resident variant (chain on a dedicated CTA of a 3-CTA cluster;
-    PNN_RESIDENT_V10=1) on the C4 and C2 shapes with ragged and short slices."""
-    monkeypatch.setenv("PNN_RESIDENT_V10", "1")
+def test_resident_v10_split_variant(orc):
+    """The v10 resident variant (chain on a dedicated CTA of a 3-CTA cluster) on the C4
+    and C2 shapes with ragged and short slices."""
     for name, K, n in [("C4", 16, 16 * 70 + 5), ("C2", 4, 4 * 300 + 3), ("C4", 6, 6 * 3 + 1)]:
         c = CONFIGS[name]
         X, y = make_split(n, "train", 0)
-        _, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, 1, "resident")
+        net, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, 1, "resident", variant="v10")
+        assert net.kernel_variant() == 10
         okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, threads=8)
         assert np.abs(kids - okids).max() < TOL, name
         assert np.abs(merged - omerged).max() < TOL, name
+
+
+TMEM_CASES = [  # (config, activations, K, rows): C4 ragged, C2 (H = 100, sigmoid/½-SSE), every pair
+    ("C4", None, 40, 40 * 90 + 7),
+    ("C2", None, 4, 4 * 400 + 3),
+    ("C4", ["tanh", "softmax"], 8, 8 * 60 + 1),
+    ("C4", ["sigmoid", "softmax"], 8, 8 * 60 + 1),
+    ("C4", ["tanh", "tanh"], 8, 8 * 60 + 1),
+    ("C4", ["relu", "sigmoid"], 8, 8 * 60 + 1),
+    ("C4", ["leaky_relu", "softmax"], 8, 8 * 60 + 1),
+]
+
+
+@pytest.mark.parametrize("name,act,K,n", TMEM_CASES)
+def test_resident_tmem_variant(orc, name, act, K, n):
+    """The TMEM resident variant (v11, k_tmem.cu: one SM per CN, W1 rows in registers
+    and tensor memory, the R27 Gram terms formed in the launch) vs the oracle."""
+    c = CONFIGS[name]
+    act = act or c.act
+    X, y = make_split(n, "train", 0)
+    net, kids, merged = _train(c.layers, act, c.init, K, c.lr, X, y, 1, "resident", variant="tmem")
+    assert net.kernel_variant() == 11 and net.kernel_info() == (2, 1)
+    okids, omerged = orc.train_pnn(c.layers, act, c.init, K, c.lr, 0, X, y, threads=8)
+    err = np.abs(kids - okids).max(axis=1)
+    assert err.max() < TOL, f"per-CN max-abs {err}"
+    assert np.abs(merged - omerged).max() < TOL
 
 
 def test_kernel_timing_hook():
@@ -259,20 +287,18 @@ def test_k1_is_snn_and_duplicated_shards(orc):
     np.testing.assert_array_equal(merged, kids[0])
 
 
-# (kernel, PNN_MBRES, expected kernel id): reference; AUTO = the persistent resident mini-batch
-# kernel (6); AUTO with PNN_MBRES=0 = the fp32 step kernels (4)
-MB_KERNELS = [("reference", None, 1), ("auto", None, 6), ("auto", "0", 4)]
+# (kernel, variant, expected kernel id): reference; AUTO = the persistent resident mini-batch
+# kernel (6); the mb_step variant = the fp32 step kernels (4)
+MB_KERNELS = [("reference", None, 1), ("auto", None, 6), ("auto", "mb_step", 4)]
 
 
 @pytest.mark.parametrize("kernel,mbres,kid", MB_KERNELS)
-def test_minibatch_fp32(orc, kernel, mbres, kid, monkeypatch):
+def test_minibatch_fp32(orc, kernel, mbres, kid):
     """Mini-batch GD, B=8 with a short last batch (R14), on the
     reference kernel, the resident mini-batch kernel and the fp32 step kernels."""
-    if mbres is not None:
-        monkeypatch.setenv("PNN_MBRES", mbres)
     c = CONFIGS["C4"]
     X, y = make_split(4 * 61, "train", 0)
-    net, kids, merged = _train(c.layers, c.act, c.init, 4, c.lr, X, y, batch=8, kernel=kernel)
+    net, kids, merged = _train(c.layers, c.act, c.init, 4, c.lr, X, y, batch=8, kernel=kernel, variant=mbres)
     assert net.kernel_info()[0] == kid
     okids, omerged = orc.train_pnn(c.layers, c.act, c.init, 4, c.lr, 0, X, y, batch=8)
     assert np.abs(kids - okids).max() < TOL
@@ -280,16 +306,15 @@ def test_minibatch_fp32(orc, kernel, mbres, kid, monkeypatch):
 
 
 @pytest.mark.parametrize("kernel,mbres,kid", MB_KERNELS)
-def test_f1_paper_workload_reduced(orc, kernel, mbres, kid, monkeypatch):
+def test_f1_paper_workload_reduced(orc, kernel, mbres, kid):
     """f1: the paper's own setting (784-256-10 ReLU/softmax, N(0,1) init, fp32
     mini-batch B=50, η 0.1) on 3 CNs with ragged
     slices and a short last batch, 2 epochs, vs the oracle."""
-    if mbres is not None:
-        monkeypatch.setenv("PNN_MBRES", mbres)
     c = CONFIGS["F1"]
     K, n = 3, 3 * (50 * 3 + 17) + 2
     X, y = make_split(n, "train", 0)
-    net, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, epochs=2, batch=c.batch, kernel=kernel)
+    net, kids, merged = _train(c.layers, c.act, c.init, K, c.lr, X, y, epochs=2, batch=c.batch, kernel=kernel,
+                               variant=mbres)
     assert net.kernel_info()[0] == kid
     okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=2, batch=c.batch,
                                    threads=K)
