@@ -97,13 +97,24 @@ class ClockSampler:
                 "n_samples": len(self.samples)}
 
 
-def _oracle_sample(cfg, budget_s):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_sample(cfg, budget_s, cores=None):
     """Pick a bounded sample of the workload's CNs (≈budget_s of CPU work on
-    the host cores, ~1.2 GFLOP/s/core scalar fp32) and pre-generate its rows."""
+    `cores` host cores (default: all), ~1.2 GFLOP/s/core scalar fp32) and
+    pre-generate its rows."""
     import oracle
     from datagen import make_rows
     oracle.build()
-    cores = len(os.sched_getaffinity(0))
+    cores = cores or len(os.sched_getaffinity(0))
     start, count = oracle.shard_bounds(cfg.n_train, cfg.K)
     S = int(count[0])
     per_cn = S * cfg.epochs * fma_per_sample(cfg.layers) * 2 / 1.0e9      # GFLOP per CN
@@ -150,7 +161,7 @@ def run_reference(args, cfg):
         "config": {"workload": cfg.name, "layers": list(cfg.layers), "K": cfg.K,
                    "rows": cfg.n_train, "epochs": cfg.epochs, "batch": cfg.batch},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "oracle",
-                         "sample": desc},
+                         "sample": desc, "cpu_model": cpu_model(), "host_cores": len(os.sched_getaffinity(0))},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -160,8 +171,14 @@ def cpu_baseline(cfg, budget_s=12.0):
     t0 = time.perf_counter()
     run()
     t = time.perf_counter() - t0
+    run1, units1, _, desc1 = _oracle_sample(cfg, 3.0, cores=1)      # the same oracle on one core
+    t1 = time.perf_counter()
+    run1()
+    t1 = time.perf_counter() - t1
     return {"value": units / t, "unit": "samples/s", "cores": threads, "kind": "oracle",
-            "sample": desc + f" ({t:.1f} s wall)"}
+            "sample": desc + f" ({t:.1f} s wall)", "cpu_model": cpu_model(),
+            "host_cores": len(os.sched_getaffinity(0)), "single_core_value": units1 / t1,
+            "single_core_sample": desc1 + f" ({t1:.1f} s wall)"}
 
 
 def main():
@@ -196,6 +213,7 @@ def main():
 
     torch.cuda.set_device(local_rank)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")      # the driver counts the ranks in NCCL's log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     first, K_local = rank_subnets(cfg.K, world, rank)
     r0, nrows = rank_rows(cfg.n_train, cfg.K, world, rank)

@@ -146,14 +146,18 @@ pnn_status pnn_create(const int32_t* layers, int32_t n_layers, const int32_t* ac
                       int32_t init, int32_t n_subnets, float lr, uint64_t seed, pnn_net* out);
 
 /* Multi-GPU (SPMD over ranks, one process per GPU): this rank owns CNs
- * [floor(rank*K/nranks), floor((rank+1)*K/nranks)) and pnn_merge finishes with
- * one NCCL all-reduce over the nranks ranks.  nccl_unique_id points to the
+ * [floor(rank*K/nranks), floor((rank+1)*K/nranks)) and trains on exactly their
+ * slices (pnn_local_rows says which rows of the full set); pnn_merge finishes
+ * with one NCCL all-reduce over the nranks ranks.  nccl_unique_id points to the
  * 128-byte ncclUniqueId every rank received (e.g. via torch.distributed
- * broadcast).  nranks == 1 needs no id (may be NULL) and uses no NCCL.
- * Re-initialises the local CN slabs to the init.  Collective over ranks,
- * synchronous.  Errors: PNN_ERR_INVALID (nranks < 1, rank out of range, id
- * NULL with nranks > 1), PNN_ERR_NCCL (libnccl.so.2 missing or init failed),
- * PNN_ERR_OOM.                                                               */
+ * broadcast).  nranks == 1 needs no id (may be NULL) and uses no NCCL.  With
+ * nranks > 1 and id == NULL the rank bookkeeping applies but no communicator
+ * is made: the caller reduces itself (pnn_merge_partial → its own all-reduce of
+ * the fp64 sums → pnn_merge_finish) and pnn_merge returns PNN_ERR_STATE.  A rank
+ * that owns no CN (K < nranks) trains nothing and contributes zeros.
+ * Re-initialises the local CN slabs to the init.  Collective over ranks (with an
+ * id), synchronous.  Errors: PNN_ERR_INVALID (nranks < 1, rank out of range),
+ * PNN_ERR_NCCL (libnccl.so.2 missing or init failed), PNN_ERR_OOM.            */
 pnn_status pnn_set_comm(pnn_net net, const void* nccl_unique_id, int32_t nranks, int32_t rank);
 
 /* Update schedule: batch = 1 is stochastic GD (the default:
@@ -222,7 +226,8 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* x_host, const int32_t*
  * R18).  The local sum runs in ascending CN order in fp64, the cross-rank sum
  * is one ncclAllReduce(sum, fp64) (nranks > 1 only), then ÷K and one
  * rounding to fp32.  CNs are left untouched.  Asynchronous.
- * Errors: PNN_ERR_STATE, PNN_ERR_CUDA, PNN_ERR_NCCL.                         */
+ * Errors: PNN_ERR_STATE (also: nranks > 1 without a communicator), PNN_ERR_CUDA,
+ * PNN_ERR_NCCL.                                                              */
 pnn_status pnn_merge(pnn_net net, void* cuda_stream);
 
 /* The two device steps of pnn_merge around its all-reduce, for callers that run

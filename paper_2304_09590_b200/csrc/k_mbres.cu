@@ -12,8 +12,8 @@
 //   P3  z2 = b2 + Σ_cta partials (fixed order), softmax / φ2, δ2_b           (Eqs.4-5, 9-10)
 //   P4  δ1_b = (W²ᵀδ2_b) ⊙ φ1'(h_b) with the pre-update W² (R6); then
 //       W² −= η·Σ_b δ2_b h_bᵀ / bsz, b2 −= η·Σ_b δ2_b / bsz, b1 −= η·Σ_b δ1_b / bsz
-//   P5  W¹ −= η·Σ_b δ1_b x_bᵀ / bsz, applied row by row of the batch as
-//       w += (−η δ1_b / bsz)·x_b (fp32 rounding order differs from sum-then-scale)
+//   P5  W¹ −= η·(Σ_b δ1_b x_bᵀ) / bsz: the sum accumulates in tensor memory in ascending
+//       batch order (the oracle's association), then one scaled update per weight
 // x rows stream HBM/L2 → shared memory twice per step (P1 and P5) through a 16-slot ring of
 // 1-D bulk copies (cp.async.bulk + mbarrier complete_tx; slots released by an 8-warp
 // mbarrier).  No launches per step: the step loop lives in the kernel.
@@ -23,6 +23,7 @@
 #include "pnn_internal.h"
 #include "pnn_device.cuh"
 #include "pnn_ptx.cuh"
+#include "pnn_tmem.cuh"
 
 extern long long* g_trace;   // debug timeline (k_resident.cu; tools/trace_mbres.py)
 
@@ -56,6 +57,7 @@ struct __align__(16) MSmem {
     float b1s[UC];
     float b2s[OM];
     int lab[BMX];                     // labels of the step's batch
+    uint32_t tbase;                   // TMEM: the W¹ gradient sums of the step
 };
 constexpr size_t kHead = ((sizeof(MSmem) + 127) / 128) * 128;
 constexpr size_t kSmem = kHead + sizeof(float) * (size_t)S * DP;
@@ -115,7 +117,8 @@ mbres_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ 
     const float* Xc = X + row0 * (long long)D;
     const uint32_t xbytes = (uint32_t)D * 4u;
 
-    if (tid == 0) {
+    if (warp == 0) tmem::alloc(&sm.tbase, 256);
+    if (tid == 32) {
         for (int i = 0; i < NG; ++i) {
             mbar_init(&sm.xfull[i], 1);
             mbar_init(&sm.xempty[i], NW);
@@ -133,8 +136,12 @@ mbres_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ 
     for (int i = tid; i < OM; i += blockDim.x) sm.b2s[i] = (i < O) ? b2g[i] : 0.f;
     for (int i = tid; i < BMX * OM; i += blockDim.x) (&sm.d2[0][0])[i] = 0.f;
     fence_proxy_async_smem();
+    tmem::fence_before();
     __syncthreads();
+    tmem::fence_after();
     if constexpr (C > 1) cluster_sync_all();
+    // this warp's TMEM columns: lane quadrant warp & 3, columns 128·(warp >> 2) .. +104
+    const uint32_t tg = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 128u * (uint32_t)(warp >> 2);
 
     // ---- the x stream in groups of G = 4 batch rows: per step, pass 0 (P1) then pass 1 (P5)
     //      each stream ⌈bsz/4⌉ groups (the last group's missing rows repeat the batch's last
@@ -367,50 +374,101 @@ mbres_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ 
             sm.b2s[o] -= lr * ((g0 + g1) * invb);
         }
         MTR(7);
-        // ---------------- P5: W¹ −= η/bsz · Σ_b δ1_b x_bᵀ, batch row by batch row ----------------
-        const float nl = -lr * invb;
+        // ---------------- P5: W¹ −= η · (Σ_b δ1_b x_bᵀ) / bsz: the batch sum first ----------------
+        // The gradient sum accumulates in tensor memory (this warp's 4 rows: quad q at
+        // columns 16q + 4r, the tail lane's 8 columns at 96), in ascending batch order, then
+        // one scaled update per weight ("the gradients … are averaged before the
+        // updates"; the oracle's association order, R14).
+        {
+            uint32_t z[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) z[c] = 0u;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) tmem::st16(tg + 16 * q, z);
+            tmem::st8(tg + 96, z);
+            tmem::wait_st();
+        }
         for (int i = 0; i < nb4; ++i) {
             const float* xg = consume();
-            float cr[G][R];                        // −η δ1[b][row] / bsz (0 for masked rows)
+            float cr[G][R];                        // δ1[b][row] (0 for masked rows)
 #pragma unroll
             for (int s2 = 0; s2 < G; ++s2) {
                 const int b = G * i + s2;
                 float4 dv = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (b < bsz) dv = *reinterpret_cast<const float4*>(&sm.d1[b][kr0]);
-                cr[s2][0] = nl * dv.x; cr[s2][1] = nl * dv.y; cr[s2][2] = nl * dv.z; cr[s2][3] = nl * dv.w;
+                cr[s2][0] = dv.x; cr[s2][1] = dv.y; cr[s2][2] = dv.z; cr[s2][3] = dv.w;
             }
             uint64_t xa[G], xb[G];
 #pragma unroll
             for (int s2 = 0; s2 < G; ++s2) lds4(xg + s2 * DP + 4 * lane, xa[s2], xb[s2]);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
+                uint32_t ta[16];
+                tmem::ld16(tg + 16 * q, ta);
                 uint64_t na[G], nb[G];
 #pragma unroll
                 for (int s2 = 0; s2 < G; ++s2) {
                     na[s2] = 0ull; nb[s2] = 0ull;
                     if (q + 1 < NQ) lds4(xg + s2 * DP + 4 * lane + 128 * (q + 1), na[s2], nb[s2]);
                 }
+                tmem::wait_ld_regs<16>(ta);
 #pragma unroll
-                for (int s2 = 0; s2 < G; ++s2)
+                for (int r = 0; r < R; ++r) {
+                    uint64_t ga = pk(__uint_as_float(ta[4 * r]), __uint_as_float(ta[4 * r + 1]));
+                    uint64_t gb = pk(__uint_as_float(ta[4 * r + 2]), __uint_as_float(ta[4 * r + 3]));
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        w[r][2 * q] = ffma2(pk(cr[s2][r], cr[s2][r]), xa[s2], w[r][2 * q]);
-                        w[r][2 * q + 1] = ffma2(pk(cr[s2][r], cr[s2][r]), xb[s2], w[r][2 * q + 1]);
+                    for (int s2 = 0; s2 < G; ++s2) {
+                        ga = ffma2(pk(cr[s2][r], cr[s2][r]), xa[s2], ga);
+                        gb = ffma2(pk(cr[s2][r], cr[s2][r]), xb[s2], gb);
                     }
+                    float a0, a1, b0, b1;
+                    upk(ga, a0, a1);
+                    upk(gb, b0, b1);
+                    ta[4 * r] = __float_as_uint(a0); ta[4 * r + 1] = __float_as_uint(a1);
+                    ta[4 * r + 2] = __float_as_uint(b0); ta[4 * r + 3] = __float_as_uint(b1);
+                }
+                tmem::st16(tg + 16 * q, ta);
 #pragma unroll
                 for (int s2 = 0; s2 < G; ++s2) { xa[s2] = na[s2]; xb[s2] = nb[s2]; }
             }
+            {
+                uint32_t tt[8];
+                tmem::ld8(tg + 96, tt);
+                tmem::wait_ld_regs<8>(tt);
 #pragma unroll
-            for (int s2 = 0; s2 < G; ++s2) {
-                const float ct = (rt == 0) ? cr[s2][0] : (rt == 1) ? cr[s2][1] : (rt == 2) ? cr[s2][2] : cr[s2][3];
-                const float4 x0 = *reinterpret_cast<const float4*>(xg + s2 * DP + tcol);
-                const float4 x1 = *reinterpret_cast<const float4*>(xg + s2 * DP + tcol + 4);
-                wt[0] = fmaf(ct, x0.x, wt[0]); wt[1] = fmaf(ct, x0.y, wt[1]);
-                wt[2] = fmaf(ct, x0.z, wt[2]); wt[3] = fmaf(ct, x0.w, wt[3]);
-                wt[4] = fmaf(ct, x1.x, wt[4]); wt[5] = fmaf(ct, x1.y, wt[5]);
-                wt[6] = fmaf(ct, x1.z, wt[6]); wt[7] = fmaf(ct, x1.w, wt[7]);
+                for (int s2 = 0; s2 < G; ++s2) {
+                    const float ct = (rt == 0) ? cr[s2][0] : (rt == 1) ? cr[s2][1] : (rt == 2) ? cr[s2][2] : cr[s2][3];
+                    const float4 x0 = *reinterpret_cast<const float4*>(xg + s2 * DP + tcol);
+                    const float4 x1 = *reinterpret_cast<const float4*>(xg + s2 * DP + tcol + 4);
+                    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) tt[c] = __float_as_uint(fmaf(ct, xv[c], __uint_as_float(tt[c])));
+                }
+                tmem::st8(tg + 96, tt);
             }
             release();
+        }
+        tmem::wait_st();
+        {
+            const float nl = -lr * invb;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                uint32_t ta[16];
+                tmem::ld16(tg + 16 * q, ta);
+                tmem::wait_ld_regs<16>(ta);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    w[r][2 * q] = ffma2(pk(nl, nl), pk(__uint_as_float(ta[4 * r]), __uint_as_float(ta[4 * r + 1])),
+                                        w[r][2 * q]);
+                    w[r][2 * q + 1] = ffma2(pk(nl, nl), pk(__uint_as_float(ta[4 * r + 2]), __uint_as_float(ta[4 * r + 3])),
+                                            w[r][2 * q + 1]);
+                }
+            }
+            uint32_t tt[8];
+            tmem::ld8(tg + 96, tt);
+            tmem::wait_ld_regs<8>(tt);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) wt[c] = fmaf(nl, __uint_as_float(tt[c]), wt[c]);
         }
         MTR(8);
         __syncthreads();                           // W², b updates visible to the next step's P2/P1
@@ -440,6 +498,10 @@ mbres_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ 
     }
     for (int i = tid; i < own; i += blockDim.x) opaque(b1g)[k0 + i] = sm.b1s[i];
     if (crank == 0 && tid < O) opaque(b2g)[tid] = sm.b2s[tid];
+    tmem::fence_before();
+    __syncthreads();
+    tmem::fence_after();
+    if (warp == 0) tmem::dealloc(sm.tbase, 256);
     if constexpr (C > 1) cluster_sync_all();       // no CTA leaves while a peer may still st.async into it
 }
 

@@ -130,6 +130,10 @@ struct MbState {
         unsigned long long used = 0;
     } g[8];
     unsigned long long tick = 0;
+    // the persisting-L2 limit this handle raised (restored, and the persisting lines reset, at
+    // mb_destroy: the window must not outlive the handle's graphs)
+    bool l2_raised = false;
+    size_t l2_prev = 0;
 };
 
 // dynamic shared-memory opt-in of the GEMM instantiations the step uses (before any capture)
@@ -173,6 +177,12 @@ void mb_destroy(MbState* s) {
     if (s->ev_cx) cudaEventDestroy(s->ev_cx);
     if (s->ev_ob) cudaEventDestroy(s->ev_ob);
     if (s->ev_b3) cudaEventDestroy(s->ev_b3);
+    if (s->l2_raised) {
+        cudaDeviceSynchronize();                   // no graph of this handle still runs
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, s->l2_prev);
+        cudaGetLastError();
+    }
     delete s;
 }
 
@@ -494,10 +504,9 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
 // argument the launches bake in) and replayed, so the host issues one launch per epoch.
 // Keep the CNs' fp32 master slabs L2-resident across the epoch's steps (every step reads and
 // writes all of them; with the bf16 copies the working set is ~106 MB for C5 < 126 MB of L2):
-// an access-policy window on every kernel node of the graph.  PNN_L2_PERSIST=0 disables it.
-static void persist_l2(cudaGraph_t g, const void* base, size_t bytes) {
-    const char* env = getenv("PNN_L2_PERSIST");
-    if (env && env[0] == '0') return;
+// an access-policy window on every kernel node of the graph.  The handle restores the
+// process-wide persisting-L2 limit and resets the persisting lines when it is destroyed.
+static void persist_l2(MbState* s, cudaGraph_t g, const void* base, size_t bytes) {
     int dev = 0, maxwin = 0, maxpers = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
@@ -507,7 +516,13 @@ static void persist_l2(cudaGraph_t g, const void* base, size_t bytes) {
     size_t cur = 0;
     cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
     const size_t want = win < (size_t)maxpers ? win : (size_t)maxpers;
-    if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    if (cur < want) {
+        if (!s->l2_raised) {
+            s->l2_prev = cur;
+            s->l2_raised = true;
+        }
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    }
     size_t n = 0;
     if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess || n == 0) return;
     std::vector<cudaGraphNode_t> nodes(n);
@@ -549,7 +564,7 @@ cudaError_t launch_minibatch_bf16(MbState* s, const NetDesc& d, float* children,
         e = cudaStreamEndCapture(s->cap, &g);
         if (eq != cudaSuccess) { if (g) cudaGraphDestroy(g); return eq; }
         if (e != cudaSuccess) return e;
-        persist_l2(g, children + (long long)s_first * s->P, (size_t)s_count * (size_t)s->P * sizeof(float));
+        persist_l2(s, g, children + (long long)s_first * s->P, (size_t)s_count * (size_t)s->P * sizeof(float));
         e = cudaGraphInstantiate(&hit->exec, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) { hit->exec = nullptr; return e; }

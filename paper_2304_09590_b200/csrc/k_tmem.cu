@@ -42,6 +42,7 @@
 #include "pnn_internal.h"
 #include "pnn_device.cuh"
 #include "pnn_ptx.cuh"
+#include "pnn_tmem.cuh"
 
 extern long long* g_trace;   // debug: clock64 timeline (k_resident.cu; tools/trace_tmem.py)
 
@@ -113,59 +114,6 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
     return p;
 }
 
-// ---- tensor memory (tcgen05) ----
-__device__ __forceinline__ void tm_alloc(uint32_t* dst, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
-                 "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tm_dealloc(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// wait::ld, then tie the loaded registers to it: an empty volatile asm that "rewrites" each
-// register keeps the compiler from hoisting their uses above the wait.
-template <int N> __device__ __forceinline__ void tm_wait_ld_regs(uint32_t* a) {
-    tm_wait_ld();
-#pragma unroll
-    for (int i = 0; i < N; ++i) asm volatile("" : "+r"(a[i]));
-}
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-#define PNN_R4(a, i) "=r"(a[i]), "=r"(a[i + 1]), "=r"(a[i + 2]), "=r"(a[i + 3])
-#define PNN_W4(a, i) "r"(a[i]), "r"(a[i + 1]), "r"(a[i + 2]), "r"(a[i + 3])
-// 32 lanes × N consecutive 32-bit columns: thread t ↔ TMEM lane (lane base + t)
-__device__ __forceinline__ void tm_ld8(uint32_t t, uint32_t* a) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : PNN_R4(a, 0), PNN_R4(a, 4)
-                 : "r"(t));
-}
-__device__ __forceinline__ void tm_ld32(uint32_t t, uint32_t* a) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : PNN_R4(a, 0), PNN_R4(a, 4), PNN_R4(a, 8), PNN_R4(a, 12), PNN_R4(a, 16), PNN_R4(a, 20), PNN_R4(a, 24),
-          PNN_R4(a, 28)
-        : "r"(t));
-}
-__device__ __forceinline__ void tm_st8(uint32_t t, const uint32_t* a) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(t), PNN_W4(a, 0),
-                 PNN_W4(a, 4)
-                 : "memory");
-}
-__device__ __forceinline__ void tm_st32(uint32_t t, const uint32_t* a) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(t),
-        PNN_W4(a, 0), PNN_W4(a, 4), PNN_W4(a, 8), PNN_W4(a, 12), PNN_W4(a, 16), PNN_W4(a, 20), PNN_W4(a, 24),
-        PNN_W4(a, 28)
-        : "memory");
-}
-#undef PNN_R4
-#undef PNN_W4
-
 // 16 values per lane → lane l holds the sum over the warp of value (l >> 1), halves in
 // lanes l and l^1 still to be combined (the caller adds its own term first).
 __device__ __forceinline__ float treduce16(const float (&v)[16], int lane) {
@@ -206,7 +154,7 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
     const int32_t* Yc = Y + row0;
     const uint32_t xbytes = (uint32_t)D * 4u;
 
-    if (warp == 0) tm_alloc(&sm.tbase, 512);
+    if (warp == 0) tmem::alloc(&sm.tbase, 512);
     if (threadIdx.x == 32) {
         for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
         for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NW + 2);
@@ -224,9 +172,9 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
     for (int i = threadIdx.x; i < UMAX; i += blockDim.x) sm.b1s[i] = (i < H) ? b1g[i] : 0.f;
     for (int i = threadIdx.x; i < 24; i += blockDim.x) (&sm.b2s[0][0])[i] = (i < O) ? b2g[i] : 0.f;
     fence_proxy_async_smem();
-    tm_fence_before();
+    tmem::fence_before();
     __syncthreads();
-    tm_fence_after();
+    tmem::fence_after();
     const uint32_t tq = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
     auto issue_x = [&](int u) {
         uint64_t* bar = &sm.xfull[u % S];
@@ -259,8 +207,8 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
             tv[4 * t] = __float_as_uint(a.x); tv[4 * t + 1] = __float_as_uint(a.y);
             tv[4 * t + 2] = __float_as_uint(b.x); tv[4 * t + 3] = __float_as_uint(b.y);
         }
-        tm_st32(tq + q * TQCOLS, tv);
-        tm_st8(tq + q * TQCOLS + 32, tv + 32);
+        tmem::st32(tq + q * TQCOLS, tv);
+        tmem::st8(tq + q * TQCOLS + 32, tv + 32);
     }
     const int trow = lane >> 1, th8 = lane & 1;     // tail: row kr0 + trow, columns 768 + 8·th8 .. +7
     {
@@ -270,9 +218,9 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             tt[j] = __float_as_uint((live && XC + 8 * th8 + j < D) ? src[j] : 0.f);
-        tm_st8(tq + TTAIL, tt);
+        tmem::st8(tq + TTAIL, tt);
     }
-    tm_wait_st();
+    tmem::wait_st();
 
     // chain side: warp 2p+h of pair p owns units 64h + lane and 64h + 32 + lane
     const int pair = warp >> 1, half = warp & 1;
@@ -307,8 +255,8 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 uint32_t tv[TQCOLS];
-                tm_ld32(tq + q * TQCOLS, tv);
-                tm_ld8(tq + q * TQCOLS + 32, tv + 32);
+                tmem::ld32(tq + q * TQCOLS, tv);
+                tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
                 uint64_t xa, xb;
                 lds4(xn + 128 * q, xa, xb);
                 if (q / 3 == gh) {
@@ -322,7 +270,7 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                     acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
                     acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
                 }
-                tm_wait_ld_regs<TQCOLS>(tv);
+                tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
                 for (int t = 0; t < TR; ++t) {
                     acc[RR + t] = ffma2(pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1])), xa, acc[RR + t]);
@@ -333,10 +281,10 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
             float px;
             {
                 uint32_t tt[8];
-                tm_ld8(tq + TTAIL, tt);
+                tmem::ld8(tq + TTAIL, tt);
                 const float* xt = xring + sl * DP + XC + 8 * th8;
                 const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
-                tm_wait_ld_regs<8>(tt);
+                tmem::wait_ld_regs<8>(tt);
                 px = __uint_as_float(tt[0]) * x0.x;
                 px = fmaf(__uint_as_float(tt[1]), x0.y, px); px = fmaf(__uint_as_float(tt[2]), x0.z, px);
                 px = fmaf(__uint_as_float(tt[3]), x0.w, px); px = fmaf(__uint_as_float(tt[4]), x1.x, px);
@@ -519,8 +467,8 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 uint32_t tv[TQCOLS];
-                tm_ld32(tq + q * TQCOLS, tv);
-                tm_ld8(tq + q * TQCOLS + 32, tv + 32);
+                tmem::ld32(tq + q * TQCOLS, tv);
+                tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
                 uint64_t xa, xb;
                 lds4(xo + 128 * q, xa, xb);
 #pragma unroll
@@ -528,7 +476,7 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                     w[r][2 * q] = ffma2(pk(gn[r], gn[r]), xa, w[r][2 * q]);
                     w[r][2 * q + 1] = ffma2(pk(gn[r], gn[r]), xb, w[r][2 * q + 1]);
                 }
-                tm_wait_ld_regs<TQCOLS>(tv);
+                tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
                 for (int t = 0; t < TR; ++t) {
                     const uint64_t gg = pk(gn[RR + t], gn[RR + t]);
@@ -540,22 +488,22 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                     tv[4 * t] = __float_as_uint(a0); tv[4 * t + 1] = __float_as_uint(a1);
                     tv[4 * t + 2] = __float_as_uint(b0); tv[4 * t + 3] = __float_as_uint(b1);
                 }
-                tm_st32(tq + q * TQCOLS, tv);
-                tm_st8(tq + q * TQCOLS + 32, tv + 32);
+                tmem::st32(tq + q * TQCOLS, tv);
+                tmem::st8(tq + q * TQCOLS + 32, tv + 32);
             }
             {
                 uint32_t tt[8];
-                tm_ld8(tq + TTAIL, tt);
+                tmem::ld8(tq + TTAIL, tt);
                 const float* xt = xring + (uu % S) * DP + XC + 8 * th8;
                 const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
                 const float gt = -sm.gbuf[uu % GR][kr0 + trow];
-                tm_wait_ld_regs<8>(tt);
+                tmem::wait_ld_regs<8>(tt);
                 const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
                 for (int j = 0; j < 8; ++j) tt[j] = __float_as_uint(fmaf(gt, xv[j], __uint_as_float(tt[j])));
-                tm_st8(tq + TTAIL, tt);
+                tmem::st8(tq + TTAIL, tt);
             }
-            tm_wait_st();
+            tmem::wait_st();
             TR(9);
         }
     }
@@ -573,9 +521,9 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
 #pragma unroll 1
     for (int q = 0; q < NQ; ++q) {
         uint32_t tv[TQCOLS];
-        tm_ld32(tq + q * TQCOLS, tv);
-        tm_ld8(tq + q * TQCOLS + 32, tv + 32);
-        tm_wait_ld_regs<TQCOLS>(tv);
+        tmem::ld32(tq + q * TQCOLS, tv);
+        tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
+        tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
         for (int t = 0; t < TR; ++t) {
             if (kr0 + RR + t < H) {
@@ -588,8 +536,8 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
     }
     {
         uint32_t tt[8];
-        tm_ld8(tq + TTAIL, tt);
-        tm_wait_ld_regs<8>(tt);
+        tmem::ld8(tq + TTAIL, tt);
+        tmem::wait_ld_regs<8>(tt);
         if (kr0 + trow < H) {
             float* dst = opaque(W1) + (long long)(kr0 + trow) * D + XC + 8 * th8;
 #pragma unroll
@@ -597,10 +545,10 @@ sgd_tmem_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 if (XC + 8 * th8 + j < D) dst[j] = __uint_as_float(tt[j]);
         }
     }
-    tm_fence_before();
+    tmem::fence_before();
     __syncthreads();
-    tm_fence_after();
-    if (warp == 0) tm_dealloc(sm.tbase, 512);
+    tmem::fence_after();
+    if (warp == 0) tmem::dealloc(sm.tbase, 512);
     for (int i = threadIdx.x; i < H * O; i += blockDim.x) {
         const int o = i / H, u = i % H;
         opaque(W2)[(long long)o * H + u] = sm.w2s[u][o];

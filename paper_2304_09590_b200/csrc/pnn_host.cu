@@ -44,6 +44,8 @@ struct pnn_net_s {
     int32_t* d_ystage = nullptr;
     long long stage_rows = 0;
     cudaStream_t copy_stream = nullptr;
+    cudaEvent_t stage_released = nullptr;   // recorded after the last launch that reads the staging
+                                            // buffers (any stream); copy_stream waits on it
     std::vector<float> h_init;        // init parameters (cloned into every CN)
     bool poisoned = false;
     std::string err;
@@ -361,6 +363,7 @@ pnn_status pnn_create(const int32_t* layers, int32_t n_layers, const int32_t* ac
         if (e == cudaSuccess)
             e = cudaMemcpy(net->d_merged, net->h_init.data(), sizeof(float) * d.P, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->stage_released, cudaEventDisableTiming);
         if (e != cudaSuccess)
             st = fail(net, e == cudaErrorMemoryAllocation ? PNN_ERR_OOM : PNN_ERR_CUDA, "%s",
                       cudaGetErrorString(e));
@@ -379,14 +382,14 @@ pnn_status pnn_set_comm(pnn_net net, const void* id, int32_t nranks, int32_t ran
     if (st) return st;
     if (nranks < 1 || rank < 0 || rank >= nranks)
         return fail(net, PNN_ERR_INVALID, "nranks = %d, rank = %d", nranks, rank);
-    if (nranks > 1 && !id) return fail(net, PNN_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1");
     CUDA_TRY(net, cudaSetDevice(net->device));
     if (net->comm) { g_nccl.CommDestroy((ncclComm_t)net->comm); net->comm = nullptr; }
     net->nranks = nranks;
     net->rank = rank;
     net->k_first = (int)((long long)rank * net->K / nranks);
     net->K_local = (int)((long long)(rank + 1) * net->K / nranks) - net->k_first;
-    if (nranks > 1) {
+    if (nranks > 1 && !net->d_msum) CUDA_TRY(net, cudaMalloc(&net->d_msum, sizeof(double) * net->d.P));
+    if (nranks > 1 && id) {                       // id == NULL: the caller reduces (merge_partial/finish)
         std::string why;
         if (!load_nccl(why)) return fail(net, PNN_ERR_NCCL, "%s", why.c_str());
         ncclUniqueId uid;
@@ -395,7 +398,6 @@ pnn_status pnn_set_comm(pnn_net net, const void* id, int32_t nranks, int32_t ran
         ncclResult_t r = g_nccl.CommInitRank(&comm, nranks, uid, rank);
         net->comm = comm;
         if (r != ncclSuccess) return fail(net, PNN_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
-        if (!net->d_msum) CUDA_TRY(net, cudaMalloc(&net->d_msum, sizeof(double) * net->d.P));
     }
     return alloc_local(net);
 }
@@ -539,6 +541,7 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
     CUDA_TRY(net, cudaSetDevice(net->device));
     cudaStream_t cs = (cudaStream_t)stream;
     if (net->stage_rows < n) {
+        cudaEventSynchronize(net->stage_released);   // no launch still reads the old buffers
         cudaFree(net->d_xstage); cudaFree(net->d_ystage);
         net->d_xstage = nullptr; net->d_ystage = nullptr; net->stage_rows = 0;
         CUDA_TRY(net, cudaMalloc(&net->d_xstage, sizeof(float) * (size_t)n * net->d.n[0]));
@@ -565,13 +568,28 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         groups = groups < 1 ? 1 : (groups > 8 ? 8 : groups);
     }
     const size_t row_bytes = sizeof(float) * net->d.n[0];
-    cudaEvent_t ready[8];
-    for (int g = 0; g < groups; ++g) CUDA_TRY(net, cudaEventCreateWithFlags(&ready[g], cudaEventDisableTiming));
-    // the previous epoch's kernels may still read the staging buffer
-    cudaEvent_t prev;
-    CUDA_TRY(net, cudaEventCreateWithFlags(&prev, cudaEventDisableTiming));
-    CUDA_TRY(net, cudaEventRecord(prev, cs));
-    CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, prev, 0));
+    // Events and the copy stream are released on every return path: the copies already
+    // enqueued finish before the call returns (the host buffers are consumed on return,
+    // success or not), and the staging buffers are marked busy until the last launch that
+    // reads them, on whatever stream this call used.
+    struct Guard {
+        pnn_net net;
+        cudaStream_t cs;
+        cudaEvent_t ready[8] = {};
+        int n = 0;
+        bool launched = false;
+        ~Guard() {
+            if (launched) cudaEventRecord(net->stage_released, cs);
+            cudaStreamSynchronize(net->copy_stream);
+            for (int g = 0; g < n; ++g) cudaEventDestroy(ready[g]);
+        }
+    } guard{net, cs};
+    for (int g = 0; g < groups; ++g) {
+        CUDA_TRY(net, cudaEventCreateWithFlags(&guard.ready[g], cudaEventDisableTiming));
+        guard.n = g + 1;
+    }
+    // the previous call's launches (on any stream) may still read the staging buffers
+    CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, net->stage_released, 0));
     for (int g = 0; g < groups; ++g) {
         const int s0 = (int)((long long)g * net->K_local / groups);
         const int s1 = (int)((long long)(g + 1) * net->K_local / groups);
@@ -583,14 +601,12 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
                                       row_bytes * rows, cudaMemcpyHostToDevice, net->copy_stream));
         CUDA_TRY(net, cudaMemcpyAsync(net->d_ystage + r0, yh + r0, sizeof(int32_t) * rows,
                                       cudaMemcpyHostToDevice, net->copy_stream));
-        CUDA_TRY(net, cudaEventRecord(ready[g], net->copy_stream));
-        CUDA_TRY(net, cudaStreamWaitEvent(cs, ready[g], 0));
+        CUDA_TRY(net, cudaEventRecord(guard.ready[g], net->copy_stream));
+        CUDA_TRY(net, cudaStreamWaitEvent(cs, guard.ready[g], 0));
+        guard.launched = true;
         if ((st = launch_train(net, net->d_xstage, net->d_ystage, n, s0, s1 - s0, cs))) return st;
     }
-    CUDA_TRY(net, cudaStreamSynchronize(net->copy_stream));   // host buffers consumed
-    for (int g = 0; g < groups; ++g) cudaEventDestroy(ready[g]);
-    cudaEventDestroy(prev);
-    return PNN_OK;
+    return PNN_OK;                                 // (the guard waits for the copies)
 }
 
 pnn_status pnn_merge(pnn_net net, void* stream) {
@@ -603,6 +619,9 @@ pnn_status pnn_merge(pnn_net net, void* stream) {
         CUDA_TRY(net, launch_merge_local(net->d_children, net->K_local, P, net->K, net->d_merged, cs));
         return PNN_OK;
     }
+    if (!net->comm)
+        return fail(net, PNN_ERR_STATE, "nranks = %d without an NCCL communicator: reduce with "
+                    "pnn_merge_partial + an all-reduce + pnn_merge_finish", net->nranks);
     CUDA_TRY(net, launch_merge_sum(net->d_children, net->K_local, P, net->d_msum, cs));
     ncclResult_t r = g_nccl.AllReduce(net->d_msum, net->d_msum, (size_t)P, ncclFloat64, ncclSum,
                                       (ncclComm_t)net->comm, cs);
@@ -777,6 +796,7 @@ pnn_status pnn_destroy(pnn_net net) {
     cudaFree(net->d_xstage);
     cudaFree(net->d_ystage);
     if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
+    if (net->stage_released) cudaEventDestroy(net->stage_released);
     delete net;
     return PNN_OK;
 }

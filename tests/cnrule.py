@@ -1,0 +1,67 @@
+"""The per-CN parity rule of the fp32 paths — test infrastructure (DESIGN.md §3 R22/R24).
+
+north_star: every weight and bias of every CN and of the merged net within max-abs 1e-4
+of the fp32 oracle.  A CN over that bar passes only with a recorded cause:
+  * ReLU-family hidden layers (Eq.4's branch point): a logged kink at
+    the first divergent step (R24, tests/kinks.py) — a pre-activation within 1e-5 of 0
+    whose sign the two sides' rounding decides differently;
+  * otherwise (smooth hidden layers, or a ReLU CN whose divergence grows gradually with
+    no kink — N(0,1)-init nets at η = 0.1 are as ill-conditioned in fp32 as C2): the
+    CN's error is inside the fp32 envelope of its slice
+    (R22, tests/envelope.py): no larger than the oracle's own spread under 1-ulp
+    perturbations of its inputs (64 trials: a further valid trajectory lands outside with
+    probability ~1/65) or the spread of another valid fp32
+    ordering (torch, per-sample SGD only).
+The merged net is the mean of the children, so its bound is the mean of their bounds.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+TOL = 1e-4
+RELU_FAMILY = ("relu", "leaky_relu")
+
+
+def _kernel_name(kid):
+    return {1: "reference", 2: "resident", 5: "cluster"}.get(int(kid), "auto")
+
+
+def cn_bound(orc, net, layers, act, init, lr, Xi, yi, err, okid, epochs, batch=1):
+    """(bound, info) for one CN whose max-abs error is `err`."""
+    if err < TOL:
+        return TOL, None
+    p0 = orc.init_params(layers, init, 0)
+    info = {}
+    if any(a in RELU_FAMILY for a in act[:-1]):
+        from tests.kinks import find_kink, has_kink
+        kr = find_kink(orc, list(layers), list(act), lr, p0, Xi, yi, epochs, variant=net.kernel_variant(),
+                       kernel=_kernel_name(net.kernel_info()[0]), batch=batch)
+        info = {"kink": kr, "kink_logged": has_kink(kr)}
+        if has_kink(kr):
+            return err, info
+        # no kink: a gradual divergence — the slice is ill-conditioned in fp32 (R22, as C2)
+    from tests.envelope import perturbation_envelope, torch_sgd_fp32
+    env = perturbation_envelope(orc, layers, act, p0, Xi, yi, lr, epochs, batch=batch)
+    if batch == 1:
+        env = max(env, float(np.abs(torch_sgd_fp32(layers, act, p0, Xi, yi, lr, epochs) - okid).max()))
+    info["envelope"] = env
+    return max(TOL, env), info
+
+
+def check_cns(orc, net, layers, act, init, K, lr, X, y, kids, okids, epochs, batch=1, log=print):
+    start, count = orc.shard_bounds(len(y), K)
+    bounds, report = [], []
+    for i in range(K):
+        err = float(np.abs(kids[i] - okids[i]).max())
+        a, b = int(start[i]), int(start[i] + count[i])
+        bound, info = cn_bound(orc, net, layers, act, init, lr, X[a:b], y[a:b], err, okids[i], epochs, batch)
+        report.append((i, err, bound, info))
+        bounds.append(bound)
+        assert err < TOL or err <= bound, f"CN {i}: max-abs {err:.3g} without a recorded cause: {info}"
+    log("per-CN (index, max-abs, bound, cause):", report)
+    return bounds
+
+
+def check_merged(merged, omerged, bounds):
+    err = float(np.abs(merged - omerged).max())
+    assert err <= float(np.mean(bounds)), f"merged max-abs {err:.3g} > mean of the per-CN bounds {np.mean(bounds):.3g}"

@@ -11,9 +11,11 @@ two valid fp32 orderings.  A second measure needs no second implementation:
 re-run the fp32 oracle from the same init perturbed by 1 ulp per parameter
 (random direction) — how far the oracle itself moves is the precision to
 which fp32 arithmetic determines the result at all (perturbation_envelope).
-DESIGN.md §3 (R22) states the rule that uses them: a CN passes if
-max-abs(GPU - oracle_fp32) <= max(1e-4, 2 * envelope), envelope = the
-largest of the torch ordering and three 1-ulp perturbation runs.
+DESIGN.md §3 (R22) states the rule that uses them (tests/cnrule.py): a CN on a
+smooth net passes if max-abs(GPU - oracle_fp32) <= max(1e-4, envelope), envelope =
+the largest of the torch ordering and 64 1-ulp perturbation runs — the GPU,
+another valid fp32 ordering, may differ from the oracle by no more than the oracle
+differs from itself when fp32 does not determine the trajectory.
 """
 import numpy as np
 import torch
@@ -59,33 +61,24 @@ def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1):
     return np.concatenate([np.concatenate([W[l].ravel().numpy(), b[l].numpy()]) for l in range(L)])
 
 
-def perturbation_envelope(orc, layers, act, params, X, y, lr, epochs=1, trials=3, seed=1, batch=1):
-    """max over `trials` of max-abs(oracle(params ± 1 ulp) - oracle(params)), fp32."""
+def perturbation_envelope(orc, layers, act, params, X, y, lr, epochs=1, trials=64, seed=1, batch=1, threads=None):
+    """max over `trials` of max-abs(oracle(params ± 1 ulp) - oracle(params)), fp32.
+
+    With T exchangeable draws, a further draw exceeds their maximum with probability
+    1/(T+1): at T = 64 a GPU result (another valid fp32 trajectory) outside the envelope
+    is a ~1.5 % event, not a tolerance factor picked by hand.  Trials run in parallel
+    (the oracle's C calls release the GIL)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
     rng = np.random.default_rng(seed)
     p0 = np.asarray(params, np.float32)
     ref = orc.train(layers, act, p0, X, y, lr, epochs, batch=batch)
-    worst = 0.0
-    for _ in range(trials):
-        direction = np.where(rng.random(p0.size) < 0.5, np.inf, -np.inf).astype(np.float32)
+    dirs = [np.where(rng.random(p0.size) < 0.5, np.inf, -np.inf).astype(np.float32) for _ in range(trials)]
+
+    def one(direction):
         pp = np.nextafter(p0, direction).astype(np.float32)
-        worst = max(worst, float(np.abs(orc.train(layers, act, pp, X, y, lr, epochs, batch=batch) - ref).max()))
-    return worst
+        return float(np.abs(orc.train(layers, act, pp, X, y, lr, epochs, batch=batch) - ref).max())
 
-
-def check_minibatch_cns(orc, layers, act, init, K, lr, X, y, kids, okids, epochs, batch, tol=1e-4):
-    """R22's per-CN rule for mini-batch runs: max-abs < tol, or <= 2x the oracle's own
-    1-ulp perturbation envelope on that CN's slice (N(0,1)-init ReLU nets are as
-    ill-conditioned in fp32 as C2)."""
-    p0 = orc.init_params(layers, init, 0)
-    start, count = orc.shard_bounds(len(y), K)
-    report = []
-    for i in range(K):
-        err = float(np.abs(kids[i] - okids[i]).max())
-        env = None
-        if err >= tol:
-            a, b = int(start[i]), int(start[i] + count[i])
-            env = perturbation_envelope(orc, layers, act, p0, X[a:b], y[a:b], lr, epochs, batch=batch)
-        report.append((i, err, env))
-        assert err < tol or err <= 2 * env, f"CN {i}: max-abs {err:.3g}, fp32 envelope {env}"
-    print("per-CN (index, max-abs vs oracle, fp32 envelope):", report)
-    return report
+    n = threads or max(1, len(os.sched_getaffinity(0)))
+    with ThreadPoolExecutor(max_workers=n) as ex:
+        return max(ex.map(one, dirs))

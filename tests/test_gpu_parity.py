@@ -318,11 +318,9 @@ def test_f1_paper_workload_reduced(orc, kernel, mbres, kid):
     assert net.kernel_info()[0] == kid
     okids, omerged = orc.train_pnn(c.layers, c.act, c.init, K, c.lr, 0, X, y, epochs=2, batch=c.batch,
                                    threads=K)
-    # R22: < 1e-4, or <= 2x the oracle's 1-ulp perturbation envelope on that CN (N(0,1) init, ReLU)
-    from tests.envelope import check_minibatch_cns
-    report = check_minibatch_cns(orc, c.layers, c.act, c.init, K, c.lr, X, y, kids, okids, 2, c.batch)
-    if all(e < TOL for _, e, _ in report):
-        assert np.abs(merged - omerged).max() < TOL
+    from tests.cnrule import check_cns, check_merged
+    bounds = check_cns(orc, net, c.layers, c.act, c.init, K, c.lr, X, y, kids, okids, 2, c.batch)
+    check_merged(merged, omerged, bounds)
 
 
 def test_error_paths():
@@ -378,63 +376,8 @@ def test_set_params_roundtrip_and_predict_subnet(orc):
     np.testing.assert_array_equal(net.get_params(-1), p)
 
 
-# ---------------------------------------------------------------------------
-# Full-size configs: the GPU trains every CN; the oracle re-trains a sample of
-# CNs one by one on their slices (the oracle cannot do all 1024 in seconds).
-# ---------------------------------------------------------------------------
-def _check_cns(orc, c, kids, okids, sample, rows, epochs):
-    """Per-CN gate: max-abs <= 1e-4, or — where fp32 itself does not determine
-    the result to 1e-4 (two valid orderings, or the oracle under 1-ulp input
-    perturbations, already disagree by more) — <= 2x that measured envelope
-    (tests/envelope.py; DESIGN.md §3 R22)."""
-    from tests.envelope import perturbation_envelope, torch_sgd_fp32
-    p0 = orc.init_params(c.layers, c.init, 0)
-    report = []
-    for j, i in enumerate(sample):
-        err = float(np.abs(kids[i] - okids[j]).max())
-        env = None
-        if err >= TOL:
-            Xi, yi = rows(i)
-            env = max(float(np.abs(torch_sgd_fp32(c.layers, c.act, p0, Xi, yi, c.lr, epochs) - okids[j]).max()),
-                      perturbation_envelope(orc, c.layers, c.act, p0, Xi, yi, c.lr, epochs))
-        report.append((i, err, env))
-        assert err < TOL or err <= 2 * env, f"CN {i}: max-abs {err:.3g}, fp32 envelope {env}"
-    print(c.name, "per-CN (index, max-abs vs oracle, fp32 envelope):", report)
-    return report
-
-
-def _full(orc, name, sample):
-    c = CONFIGS[name]
-    X, y = make_split(c.n_train, "train", 0)
-    net, kids, merged = _train(c.layers, c.act, c.init, c.K, c.lr, X, y, c.epochs)
-    okids, _ = orc.train_pnn(c.layers, c.act, c.init, c.K, c.lr, 0, X, y, epochs=c.epochs,
-                             threads=8, subnets=sample)
-    start, count = orc.shard_bounds(c.n_train, c.K)
-    rows = lambda i: (X[start[i]:start[i] + count[i]], y[start[i]:start[i] + count[i]])  # noqa: E731
-    report = _check_cns(orc, c, kids, okids, sample, rows, c.epochs)
-    np.testing.assert_array_equal(merged, orc.merge(kids))    # merge of all K children, bit-exact
-    Xt, _ = make_split(c.n_test, "test", 0)
-    lab = net.predict(dev(Xt)).cpu().numpy()
-    np.testing.assert_array_equal(lab, orc.predict(c.layers, c.act, merged, Xt))
-    return merged, okids, report
-
-
-def test_c2_full(orc):
-    merged, okids, report = _full(orc, "C2", [0, 1, 2, 3])
-    # all four CNs re-trained by the oracle: the merged network too.  The merge
-    # is the mean of the children, so its envelope is the mean of theirs (R22).
-    env = sum(max(TOL, 2 * e) if e is not None else TOL for _, _, e in report) / len(report)
-    err = float(np.abs(merged - orc.merge(okids)).max())
-    print("C2 merged max-abs", err, "bound", env)
-    assert err <= env
-
-
-def test_c3_full_sampled(orc):
-    _full(orc, "C3", [0, 31])
-
-
-def test_c4_full_sampled(orc):
-    _full(orc, "C4", [0, 1, 511, 777, 1023])
+# Full-size, full-population parity (every CN of C1-C5 vs the oracle, merged nets, R24
+# kink accounting, full-test-set labels): tests/test_gpu_fullsize.py.
 
 
 @pytest.mark.parametrize("name,K,rows,batch", [
