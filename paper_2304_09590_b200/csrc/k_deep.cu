@@ -32,6 +32,7 @@
 #include "pnn_internal.h"
 #include "pnn_device.cuh"
 #include "pnn_ptx.cuh"
+#include "pnn_tmem.cuh"
 
 extern long long* g_trace;   // debug timeline (k_resident.cu; tools/trace_deep.py)
 
@@ -39,13 +40,22 @@ namespace {
 
 using namespace ptx;
 
-constexpr int R = 8;                  // W1 rows per sweep warp
 constexpr int NSW = 5;                // sweep warps
 constexpr int NCW = 3;                // chain warps
 constexpr int NW = NSW + NCW;
-constexpr int R1MAX = R * NSW;        // layer-1 units per CTA
-constexpr int RW2 = 5;                // layer-2 rows per chain warp
-constexpr int R2MAX = RW2 * NCW;      // layer-2 units per CTA
+// Per cluster size: W¹ rows per sweep warp in registers (RR) and in tensor memory (TRW), and
+// layer-2 rows per chain warp (RW2).  C = 8: 40 register rows per CTA (the C3 shape in 3 waves
+// of at most 15 co-resident 8-CTA clusters); C = 4: 30 register + 50 TMEM rows per CTA, so the
+// C3 shape fits 4-CTA clusters and all 32 of its CNs run at once (33 co-resident).
+template <int C> struct DeepShape;
+template <> struct DeepShape<8> { static constexpr int RR = 8, TRW = 0, RW2 = 5; };
+template <> struct DeepShape<4> { static constexpr int RR = 6, TRW = 10, RW2 = 9; };
+constexpr int RPWMAX = 16;            // W¹ rows per sweep warp (max over C)
+constexpr int R1MAX = RPWMAX * NSW;   // layer-1 units per CTA (max)
+constexpr int RW2MAX = 9;
+constexpr int R2MAX = RW2MAX * NCW;   // layer-2 units per CTA (max)
+template <int C> constexpr int r1cap() { return (DeepShape<C>::RR + DeepShape<C>::TRW) * NSW; }
+template <int C> constexpr int r2cap() { return DeepShape<C>::RW2 * NCW; }
 constexpr int H1MAX = 384;            // W² row stride in shared memory (h1 padded with zeros)
 constexpr int NJ4 = H1MAX / 128;      // 16-byte column groups per lane
 constexpr int OMAX = 16;
@@ -76,12 +86,13 @@ struct __align__(16) DSmem {
     float asum[AR][R1MAX][4];
     float gbuf[GR][R1MAX];
     float b1s[R1MAX];
-    float wx[NSW][R][16];
+    float wx[NSW][RPWMAX][16];
     float h1buf[2][H1MAX];
     float zbuf[2][NGMAX][OMAX];
     float p1buf[2][NGMAX][R1MAX];
     float b2s[R2MAX + 1];
     float w3s[OMAX][R2MAX + 1];        // W³[o][r·R2 + i]
+    uint32_t tbase;                    // TMEM base (C = 4: the sweeps' TMEM rows)
 };
 constexpr size_t kHead = ((sizeof(DSmem) + 127) / 128) * 128;
 constexpr size_t kSmem = kHead + sizeof(float) * ((size_t)R2MAX * H1MAX + (size_t)S * DP);
@@ -149,6 +160,9 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int crank = (int)cluster_rank();
     const int cn = s_first + (int)(blockIdx.x / C);
+    constexpr int R = DeepShape<C>::RR;            // W¹ rows per sweep warp in registers
+    constexpr int TRW = DeepShape<C>::TRW;         // … and in tensor memory
+    constexpr int RW2 = DeepShape<C>::RW2;         // layer-2 rows per chain warp
     const int R1 = (((H1 + C - 1) / C) + 3) & ~3, k0 = crank * R1, own1 = max(0, min(R1, H1 - k0));
     const int R2 = (H2 + C - 1) / C, k02 = crank * R2, own2 = max(0, min(R2, H2 - k02));
 
@@ -166,7 +180,10 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
     const float4* Rc = rec + 2 * row0;
     const uint32_t xbytes = (uint32_t)D * 4u;
 
-    if (threadIdx.x == 0) {
+    if constexpr (TRW > 0) {
+        if (warp == 0) tmem::alloc(&sm.tbase, 512);
+    }
+    if (threadIdx.x == 32) {
         for (int i = 0; i < S; ++i) mbar_init(&sm.xfull[i], 1);
         for (int i = 0; i < AR; ++i) mbar_init(&sm.aready[i], NSW);
         for (int i = 0; i < GR; ++i) mbar_init(&sm.gready[i], NCW);
@@ -190,8 +207,11 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
         const int o = i / (R2MAX + 1), r = i - o * (R2MAX + 1);
         sm.w3s[o][r] = (o < O && r < own2) ? W3[(long long)o * H2 + k02 + r] : 0.f;
     }
+    for (int i = threadIdx.x; i < AR * R1MAX * 4; i += blockDim.x) (&sm.asum[0][0][0])[i] = 0.f;
     fence_proxy_async_smem();
+    tmem::fence_before();
     __syncthreads();
+    tmem::fence_after();
     cluster_sync_all();                            // peers' barriers exist before any st.async
     auto issue_x = [&](int u, int slot) {
         uint64_t* bar = &sm.xfull[slot];
@@ -203,8 +223,141 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
         for (int u = 0; u < PF && u < T; ++u) issue_x(u, u);   // chain step c issues x(c+PF)
 
     if (warp < NSW) {
-        // ======================= sweeps: this warp's W¹ rows =======================
-        const int kr0 = warp * R;
+        if constexpr (TRW == 0) {
+            // ======================= sweeps: this warp's W¹ rows =======================
+            const int kr0 = warp * R;
+            uint64_t w[R][NP];
+    #pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool live = kr0 + r < own1;
+                const float* src = W1 + (long long)(k0 + kr0 + r) * D;
+    #pragma unroll
+                for (int m = 0; m < NP; ++m)
+                    w[r][m] = live ? *reinterpret_cast<const uint64_t*>(src + pcol(lane, m)) : 0ull;
+            }
+            const int tr = lane >> 2, tq = lane & 3;
+            const int nx = D - XC - 4 * tq;
+            const bool xlive = kr0 + tr < own1;
+            float* wxp = &sm.wx[warp][tr][4 * tq];
+            {
+                float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float* src = W1 + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
+                if (xlive) {
+                    if (nx > 0) w4.x = src[0];
+                    if (nx > 1) w4.y = src[1];
+                    if (nx > 2) w4.z = src[2];
+                    if (nx > 3) w4.w = src[3];
+                }
+                *reinterpret_cast<float4*>(wxp) = w4;
+            }
+            __syncwarp();
+            int sx = 0;
+            for (int s = 0; s < T + LAG; ++s) {
+                if (s < T) {
+                    mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));
+                    // F(s): acc = W¹(s-L)·x(s)
+                    const float* xn = xring + sx * DP + 4 * lane;
+                    uint64_t acc[R];
+    #pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r] = 0ull;
+                    uint64_t xa, xb;
+                    lds4(xn, xa, xb);
+    #pragma unroll
+                    for (int q = 0; q < (kNoSweep ? 0 : NQ); ++q) {
+                        uint64_t na = 0ull, nb = 0ull;
+                        if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);
+    #pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
+                            acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
+                        }
+                        xa = na;
+                        xb = nb;
+                    }
+                    float px;
+                    {
+                        const float4 w4 = *reinterpret_cast<const float4*>(wxp);
+                        const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
+                        px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
+                    }
+                    float v[R];
+    #pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        float lo, hi;
+                        upk(acc[r], lo, hi);
+                        v[r] = lo + hi;
+                    }
+                    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                    float u4[4];
+    #pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+                    float u2[2];
+    #pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
+                    const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
+                    sm.asum[s % AR][kr0 + tr][tq] = part;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
+                }
+                if (s >= LAG) {
+                    // U(s): W¹ -= g(s-L)·x(s-L)ᵀ
+                    const int u = s - LAG;
+                    mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
+                    const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
+                    const float* xo = xring + su * DP + 4 * lane;
+                    const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
+                    const float4 g0 = gv[0], g1 = gv[1];
+                    const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
+                    uint64_t xa, xb;
+                    lds4(xo, xa, xb);
+    #pragma unroll
+                    for (int q = 0; q < (kNoSweep ? 0 : NQ); ++q) {
+                        uint64_t na = 0ull, nb = 0ull;
+                        if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
+    #pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
+                            w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
+                        }
+                        xa = na;
+                        xb = nb;
+                    }
+                    float4 w4 = *reinterpret_cast<const float4*>(wxp);
+                    const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
+                    const float gq = -sm.gbuf[u % GR][kr0 + tr];
+                    w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
+                    w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
+                    *reinterpret_cast<float4*>(wxp) = w4;
+                }
+                if (++sx == S) sx = 0;
+            }
+            float* W1o = opaque(W1);
+    #pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (kr0 + r < own1) {
+                    float* dst = W1o + (long long)(k0 + kr0 + r) * D;
+    #pragma unroll
+                    for (int m = 0; m < NP; ++m) *reinterpret_cast<uint64_t*>(dst + pcol(lane, m)) = w[r][m];
+                }
+            }
+            if (xlive) {
+                const float4 w4 = *reinterpret_cast<const float4*>(wxp);
+                float* dst = W1o + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
+                if (nx > 0) dst[0] = w4.x;
+                if (nx > 1) dst[1] = w4.y;
+                if (nx > 2) dst[2] = w4.z;
+                if (nx > 3) dst[3] = w4.w;
+            }
+        } else {
+        // ============= sweeps with TMEM rows (C = 4): RR register + TRW tensor-memory rows =============
+        // TMEM: lane quadrant warp & 3, columns 256·(warp >> 2); quad q of TMEM row t at q·40 + 4t
+        constexpr int RPW = R + TRW;
+        constexpr int TQC = 4 * TRW;
+        static_assert(RPW == 16 && TRW == 10, "the 16-row sweep (treduce over 16 rows, x32 + x8 TMEM loads)");
+        const uint32_t tq = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
+        const int kr0 = warp * RPW;
         uint64_t w[R][NP];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -214,20 +367,30 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
             for (int m = 0; m < NP; ++m)
                 w[r][m] = live ? *reinterpret_cast<const uint64_t*>(src + pcol(lane, m)) : 0ull;
         }
-        const int tr = lane >> 2, tq = lane & 3;
-        const int nx = D - XC - 4 * tq;
-        const bool xlive = kr0 + tr < own1;
-        float* wxp = &sm.wx[warp][tr][4 * tq];
-        {
-            float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float* src = W1 + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
-            if (xlive) {
-                if (nx > 0) w4.x = src[0];
-                if (nx > 1) w4.y = src[1];
-                if (nx > 2) w4.z = src[2];
-                if (nx > 3) w4.w = src[3];
+#pragma unroll 1
+        for (int q = 0; q < NQ; ++q) {
+            uint32_t tv[TQC];
+#pragma unroll
+            for (int t = 0; t < TRW; ++t) {
+                const bool live = kr0 + R + t < own1;
+                const float* src = W1 + (long long)(k0 + kr0 + R + t) * D + 4 * lane + 128 * q;
+                // (slabs are 8-byte aligned only: P is even)
+                const float2 a = live ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
+                const float2 b = live ? *reinterpret_cast<const float2*>(src + 2) : make_float2(0.f, 0.f);
+                tv[4 * t] = __float_as_uint(a.x); tv[4 * t + 1] = __float_as_uint(a.y);
+                tv[4 * t + 2] = __float_as_uint(b.x); tv[4 * t + 3] = __float_as_uint(b.y);
             }
-            *reinterpret_cast<float4*>(wxp) = w4;
+            tmem::st32(tq + q * TQC, tv);
+            tmem::st8(tq + q * TQC + 32, tv + 32);
+        }
+        tmem::wait_st();
+        const int trow = lane >> 1, th8 = lane & 1;   // tail: row kr0 + trow, columns 768 + 8·th8 .. +7
+        const bool xlive = kr0 + trow < own1;
+        float* wxp = &sm.wx[warp][trow][8 * th8];
+        {
+            const float* src = W1 + (long long)(k0 + kr0 + trow) * D + XC + 8 * th8;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) wxp[j] = (xlive && XC + 8 * th8 + j < D) ? src[j] : 0.f;
         }
         __syncwarp();
         int sx = 0;
@@ -236,47 +399,62 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));
                 // F(s): acc = W¹(s-L)·x(s)
                 const float* xn = xring + sx * DP + 4 * lane;
-                uint64_t acc[R];
+                uint64_t acc[RPW];
 #pragma unroll
-                for (int r = 0; r < R; ++r) acc[r] = 0ull;
-                uint64_t xa, xb;
-                lds4(xn, xa, xb);
+                for (int r = 0; r < RPW; ++r) acc[r] = 0ull;
 #pragma unroll
-                for (int q = 0; q < (kNoSweep ? 0 : NQ); ++q) {
-                    uint64_t na = 0ull, nb = 0ull;
-                    if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);
+                for (int q = 0; q < NQ; ++q) {
+                    uint32_t tv[TQC];
+                    tmem::ld32(tq + q * TQC, tv);
+                    tmem::ld8(tq + q * TQC + 32, tv + 32);
+                    uint64_t xa, xb;
+                    lds4(xn + 128 * q, xa, xb);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
                         acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
                     }
-                    xa = na;
-                    xb = nb;
+                    tmem::wait_ld_regs<TQC>(tv);
+#pragma unroll
+                    for (int t = 0; t < TRW; ++t) {
+                        acc[R + t] = ffma2(pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1])), xa, acc[R + t]);
+                        acc[R + t] = ffma2(pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3])), xb,
+                                           acc[R + t]);
+                    }
                 }
                 float px;
                 {
-                    const float4 w4 = *reinterpret_cast<const float4*>(wxp);
-                    const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
-                    px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
+                    const float4 w0 = *reinterpret_cast<const float4*>(wxp), w1 = *reinterpret_cast<const float4*>(wxp + 4);
+                    const float* xt = xring + sx * DP + XC + 8 * th8;
+                    const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
+                    px = w0.x * x0.x;
+                    px = fmaf(w0.y, x0.y, px); px = fmaf(w0.z, x0.z, px); px = fmaf(w0.w, x0.w, px);
+                    px = fmaf(w1.x, x1.x, px); px = fmaf(w1.y, x1.y, px); px = fmaf(w1.z, x1.z, px);
+                    px = fmaf(w1.w, x1.w, px);
                 }
-                float v[R];
+                float v[RPW];
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
+                for (int r = 0; r < RPW; ++r) {
                     float lo, hi;
                     upk(acc[r], lo, hi);
                     v[r] = lo + hi;
                 }
-                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                // transpose-reduce 16 row sums: lane l ends with row l >> 1, part l & 1
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+                float u8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    u8[i] = (b4 ? v[i + 8] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 8], 16);
                 float u4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
-                    u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+                    u4[i] = (b3 ? u8[i + 4] : u8[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u8[i] : u8[i + 4], 8);
                 float u2[2];
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
-                    u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
-                const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
-                sm.asum[s % AR][kr0 + tr][tq] = part;
+                    u2[i] = (b2 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b2 ? u4[i] : u4[i + 2], 4);
+                const float part = (b1 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? u2[0] : u2[1], 2) + px;
+                sm.asum[s % AR][kr0 + trow][th8] = part;   // (parts 2, 3 stay 0)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
             }
@@ -286,29 +464,54 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
                 const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
                 const float* xo = xring + su * DP + 4 * lane;
-                const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
-                const float4 g0 = gv[0], g1 = gv[1];
-                const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
-                uint64_t xa, xb;
-                lds4(xo, xa, xb);
+                float gp[RPW];
+                {
+                    const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
 #pragma unroll
-                for (int q = 0; q < (kNoSweep ? 0 : NQ); ++q) {
-                    uint64_t na = 0ull, nb = 0ull;
-                    if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
+                    for (int i = 0; i < RPW / 4; ++i) {
+                        const float4 a = gv[i];
+                        gp[4 * i] = -a.x; gp[4 * i + 1] = -a.y; gp[4 * i + 2] = -a.z; gp[4 * i + 3] = -a.w;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    uint32_t tv[TQC];
+                    tmem::ld32(tq + q * TQC, tv);
+                    tmem::ld8(tq + q * TQC + 32, tv + 32);
+                    uint64_t xa, xb;
+                    lds4(xo + 128 * q, xa, xb);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
                         w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
                     }
-                    xa = na;
-                    xb = nb;
+                    tmem::wait_ld_regs<TQC>(tv);
+#pragma unroll
+                    for (int t = 0; t < TRW; ++t) {
+                        const uint64_t gg = pk(gp[R + t], gp[R + t]);
+                        const uint64_t a = ffma2(gg, xa, pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1])));
+                        const uint64_t b = ffma2(gg, xb, pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3])));
+                        float a0, a1, b0, b1;
+                        upk(a, a0, a1);
+                        upk(b, b0, b1);
+                        tv[4 * t] = __float_as_uint(a0); tv[4 * t + 1] = __float_as_uint(a1);
+                        tv[4 * t + 2] = __float_as_uint(b0); tv[4 * t + 3] = __float_as_uint(b1);
+                    }
+                    tmem::st32(tq + q * TQC, tv);
+                    tmem::st8(tq + q * TQC + 32, tv + 32);
                 }
-                float4 w4 = *reinterpret_cast<const float4*>(wxp);
-                const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
-                const float gq = -sm.gbuf[u % GR][kr0 + tr];
-                w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
-                w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
-                *reinterpret_cast<float4*>(wxp) = w4;
+                {
+                    const float gq = -sm.gbuf[u % GR][kr0 + trow];
+                    const float* xt = xring + su * DP + XC + 8 * th8;
+                    const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
+                    float4 w0 = *reinterpret_cast<const float4*>(wxp), w1 = *reinterpret_cast<const float4*>(wxp + 4);
+                    w0.x = fmaf(gq, x0.x, w0.x); w0.y = fmaf(gq, x0.y, w0.y); w0.z = fmaf(gq, x0.z, w0.z);
+                    w0.w = fmaf(gq, x0.w, w0.w); w1.x = fmaf(gq, x1.x, w1.x); w1.y = fmaf(gq, x1.y, w1.y);
+                    w1.z = fmaf(gq, x1.z, w1.z); w1.w = fmaf(gq, x1.w, w1.w);
+                    *reinterpret_cast<float4*>(wxp) = w0;
+                    *reinterpret_cast<float4*>(wxp + 4) = w1;
+                }
+                tmem::wait_st();
             }
             if (++sx == S) sx = 0;
         }
@@ -321,13 +524,28 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 for (int m = 0; m < NP; ++m) *reinterpret_cast<uint64_t*>(dst + pcol(lane, m)) = w[r][m];
             }
         }
+#pragma unroll 1
+        for (int q = 0; q < NQ; ++q) {
+            uint32_t tv[TQC];
+            tmem::ld32(tq + q * TQC, tv);
+            tmem::ld8(tq + q * TQC + 32, tv + 32);
+            tmem::wait_ld_regs<TQC>(tv);
+#pragma unroll
+            for (int t = 0; t < TRW; ++t) {
+                if (kr0 + R + t < own1) {
+                    float* dst = W1o + (long long)(k0 + kr0 + R + t) * D + 4 * lane + 128 * q;
+                    *reinterpret_cast<float2*>(dst) = make_float2(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1]));
+                    *reinterpret_cast<float2*>(dst + 2) =
+                        make_float2(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3]));
+                }
+            }
+        }
         if (xlive) {
-            const float4 w4 = *reinterpret_cast<const float4*>(wxp);
-            float* dst = W1o + (long long)(k0 + kr0 + tr) * D + XC + 4 * tq;
-            if (nx > 0) dst[0] = w4.x;
-            if (nx > 1) dst[1] = w4.y;
-            if (nx > 2) dst[2] = w4.z;
-            if (nx > 3) dst[3] = w4.w;
+            float* dst = W1o + (long long)(k0 + kr0 + trow) * D + XC + 8 * th8;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (XC + 8 * th8 + j < D) dst[j] = wxp[j];
+        }
         }
     } else {
         // ======================= the chain =======================
@@ -395,7 +613,7 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 z += sm.b1s[ct];
                 h1u = act_fast<A1>(z);
             }
-            if (cw < 2) {                              // units 0..39 live in warps 5 and 6
+            if (cw * 32 < own1) {                      // the chain threads that own layer-1 units
                 float4 v;
                 v.x = __shfl_sync(0xffffffffu, h1u, l4);
                 v.y = __shfl_sync(0xffffffffu, h1u, l4 + 1);
@@ -567,6 +785,12 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
         }
         if (crank == 0 && cw == 0 && lane < O) opaque(b3g)[lane] = b3r;
     }
+    if constexpr (TRW > 0) {
+        tmem::fence_before();
+        __syncthreads();
+        tmem::fence_after();
+        if (warp == 0) tmem::dealloc(sm.tbase, 512);
+    }
     cluster_sync_all();                            // no CTA leaves while a peer may still st.async into it
 }
 
@@ -610,8 +834,11 @@ cudaError_t launch_c(const NetDesc& d, float* children, const float* x, const fl
 }
 
 int deep_cluster(const NetDesc& d) {
-    for (int c = 4; c <= CMAX; c *= 2)
-        if ((d.n[1] + c - 1) / c <= R1MAX && (d.n[2] + c - 1) / c <= R2MAX) return c;
+    // the smallest cluster whose CTAs hold the layers (R1 rounded to a multiple of 4, as the
+    // kernel does): fewer SMs per CN, more CNs at once
+    auto r1 = [&](int c) { return (((d.n[1] + c - 1) / c) + 3) & ~3; };
+    if (r1(4) <= r1cap<4>() && (d.n[2] + 3) / 4 <= r2cap<4>()) return 4;
+    if (r1(8) <= r1cap<8>() && (d.n[2] + 7) / 8 <= r2cap<8>()) return 8;
     return 0;
 }
 
@@ -622,7 +849,7 @@ const char* deep_plan(const NetDesc& d, int batch) {
     if (d.L != 3) return "3-layer nets only";
     const int D = d.n[0];
     if (D % 4 != 0 || D <= XC || D > XC + 16) return "built for 768 < inputs <= 784, a multiple of 4";
-    if (d.n[1] > CMAX * R1MAX) return "first hidden layer wider than 320";
+    if (d.n[1] > 320) return "first hidden layer wider than 320";
     if (d.n[3] > OMAX) return "more than 16 outputs";
     if (d.P % 2 != 0) return "odd parameter count (W1 rows are moved as 8-byte pairs)";
     if (!deep_cluster(d)) return "hidden layers too wide for 8 CTAs";
@@ -672,13 +899,7 @@ extern "C" int pnn_debug_deep_max_clusters(int C) {
     };
     switch (C) {
     case 4: e = q(sgd_deep_kernel<4, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
-    case 5: e = q(sgd_deep_kernel<5, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
-    case 6: e = q(sgd_deep_kernel<6, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
-    case 7: e = q(sgd_deep_kernel<7, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
     case 8: e = q(sgd_deep_kernel<8, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
-    case 10: e = q(sgd_deep_kernel<10, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
-    case 12: e = q(sgd_deep_kernel<12, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
-    case 16: e = q(sgd_deep_kernel<16, PNN_TANH, PNN_TANH, PNN_SOFTMAX>); break;
     default: return -1;
     }
     return e == cudaSuccess ? n : -(int)e;
