@@ -66,31 +66,8 @@ constexpr int GR = 8;         // g ring slots (> LAG)
 static_assert(AR > LAG + 1 && GR > LAG, "ring sizes");
 constexpr int ZS = 4;         // partial-logit ring slots
 constexpr int CMAX = 4;       // cluster size
-#ifndef PNN_EXP_CHAIN_PAIRS
-#define PNN_EXP_CHAIN_PAIRS 4
-#endif
-#ifndef PNN_V8_SAME_ORDER
-#define PNN_V8_SAME_ORDER 0
-#endif
-// every warp runs F then U (instead of warps 4..7 running U before F)
-constexpr bool kV8SameOrder = PNN_V8_SAME_ORDER != 0;
-#ifndef PNN_SWEEP_XWAIT
-#define PNN_SWEEP_XWAIT 1
-#endif
-// paired sweeps: F / U for two samples per pass over the W¹ registers (5 Gram terms)
-#ifndef PNN_V8_PAIRS
-#define PNN_V8_PAIRS 1
-#endif
-#ifndef PNN_V8P_STAGGER
-#define PNN_V8P_STAGGER 0   // warps 4-7 U before F: measured slower (51.7 vs 67.4 M)
-#endif
-constexpr bool kStagger = PNN_V8P_STAGGER != 0;
 // the chain warp of the pair that does not issue the x prefetch updates b2
-constexpr int kB2Half = PNN_SWEEP_XWAIT ? 1 : 0;
-// warp pairs that take turns running the chain: the highest-numbered ones (the warp
-// scheduler favours higher warp ids within an SM sub-partition)
-constexpr int kChainPairs = PNN_EXP_CHAIN_PAIRS;
-static_assert(kChainPairs == 1 || kChainPairs == 2 || kChainPairs == 4, "chain pairs");
+constexpr int kB2Half = 1;
 constexpr int kTraceT = 64, kTraceP = 16;   // debug timeline: [cta][warp][t][point]
 
 struct __align__(16) Smem {
@@ -329,7 +306,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     constexpr uint32_t kZStride = 2 * CMAX * 16 * 4;
     constexpr uint32_t kZfullOff = (uint32_t)offsetof(Smem, zfull) - (uint32_t)offsetof(Smem, zbuf);
 
-#if PNN_V8_PAIRS
     // ===== paired sweeps: step p runs F for samples 2p, 2p+1 with W¹(2p-L) (one pass over the
     // registers for both: 32 fma.rn.f32x2 per pair of x quads), U for samples 2p-4, 2p-3, and
     // the chains of samples 2p-2, 2p-1 on their warp pairs.  Sample 2p+1's forward misses
@@ -390,8 +366,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
     for (int p = 0; p < npair + 3; ++p) {
         const int s = 2 * p;                       // (TR's index)
         TR(0);
-        __syncwarp();
-        if (kStagger && warp >= 4) u_pair(p);
         __syncwarp();
         if (p < npair) {
             // ---------------- F(2p), F(2p+1) ----------------
@@ -468,7 +442,7 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 #pragma unroll 1
         for (int cc = 0; cc < 2; ++cc) {
         const int c = 2 * p - 2 + cc;
-        if (c >= 0 && c < T && (c % kChainPairs) + (4 - kChainPairs) == (warp >> 1)) {
+        if (c >= 0 && c < T && (c & 3) == (warp >> 1)) {
             const int cs = c % S;                  // ring slot of x(c)
             // every warp's row sums of c and the end of chain c-1 (W2, b, g history in shared memory)
             mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
@@ -478,391 +452,9 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             const int label = __float_as_int(xring[cs * DP + GOFF + 4]);
             const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][uc][0]);
             float z = (pa.x + pa.y) + (pa.z + pa.w);
-            // F-before-U rows (warps 0-3: half 0) miss 4 (+1 odd) updates, U-first rows 2 (+1 odd)
-            const bool fu = !kStagger || half == 0;
-            if (fu && (c & 1)) z = fmaf(-sm.gbuf[(c + GR - 5) % GR][uc], xring[cs * DP + GOFF + 5], z);
-            if (fu) z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);
-            if (fu || (c & 1)) z = fmaf(-sm.gbuf[(c + GR - 3) % GR][uc], G.y, z);
-            z = fmaf(-sm.gbuf[(c + GR - 2) % GR][uc], G.z, z);
-            z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
-            z += sm.b1s[uc];
-            const float h = lc ? act_fwd_t<A1>(z) : 0.f;
-            TR(7);
-            // W2[o][uc] (pre-update: R6), kept for δ1 below
-            float wv[12];
-            const int zs = c % ZS;
-            {
-                const float4* wq = reinterpret_cast<const float4*>(&sm.w2s[uc][0]);
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const float4 f = wq[q];
-                    wv[4 * q] = f.x; wv[4 * q + 1] = f.y; wv[4 * q + 2] = f.z; wv[4 * q + 3] = f.w;
-                }
-            }
-            // ---- this warp's partial logits Σ_u W2[o][u] h_u: transpose-reduce over lanes ----
-            float pv0;
-            {
-                float pv[16];
-#pragma unroll
-                for (int o = 0; o < 16; ++o) pv[o] = (o < O) ? wv[o < O ? o : 0] * h : 0.f;
-                const bool c4 = lane & 16, c3 = lane & 8, c2 = lane & 4, c1 = lane & 2;
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    pv[i] = (c4 ? pv[i + 8] : pv[i]) + __shfl_xor_sync(0xffffffffu, c4 ? pv[i] : pv[i + 8], 16);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    pv[i] = (c3 ? pv[i + 4] : pv[i]) + __shfl_xor_sync(0xffffffffu, c3 ? pv[i] : pv[i + 4], 8);
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-                    pv[i] = (c2 ? pv[i + 2] : pv[i]) + __shfl_xor_sync(0xffffffffu, c2 ? pv[i] : pv[i + 2], 4);
-                pv0 = (c1 ? pv[1] : pv[0]) + __shfl_xor_sync(0xffffffffu, c1 ? pv[0] : pv[1], 2);
-                pv0 += __shfl_xor_sync(0xffffffffu, pv0, 1);
-            }
-            TR(8);
-            // lane l now holds output (l >> 1) = 8·c4 + 4·c3 + 2·c2 + c1
-            {
-                const int oi = lane >> 1;
-                const bool pub = (lane & 1) == 0 && oi < O;
-                if (pub) sm.zbuf[zs][zrow][oi] = pv0;
-                if constexpr (C > 1) {
-#pragma unroll
-                    for (int p = 0; p < C - 1; ++p)
-                        st_async_f32_if(pub, rz[p] + zs * kZStride + oi * 4, pv0,
-                                        rz[p] + kZfullOff - (uint32_t)(zrow * 64) + zs * 8);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (C > 1) mbar_arrive_expect_tx(&sm.zfull[zs], (uint32_t)((C - 1) * O * 4));
-                    else mbar_arrive(&sm.zfull[zs]);
-                }
-            }
-            TR(9);
-            // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
-            //      which comes after their wait on gready(c) (first warp of the pair) ----
-            // every warp has passed U(c-1) (aready(c) above): the slot of x(c-1-L) is free for x(c+PF)
-#if !PNN_SWEEP_XWAIT
-            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
-            if (half == 0 && c + 2 + LAG < T) {
-                const int u = c + 2 + LAG;
-                mbar_wait(&sm.xfull[(cs + 2 + LAG) % S], (uint32_t)((u / S) & 1));
-            }
-#endif
-            TR(4);
-            // ---- δ2(c) in every lane: z2 = Σ partials + b2(c) ----
-            mbar_wait(&sm.zfull[zs], (uint32_t)((c / ZS) & 1));
-            TR(5);
-            float dl[O];
-            {
-                float z2[12];
-                {
-                    const float4* bq = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        const float4 f = bq[q];
-                        z2[4 * q] = f.x; z2[4 * q + 1] = f.y; z2[4 * q + 2] = f.z; z2[4 * q + 3] = f.w;
-                    }
-                }
-                float zp[12];
-#pragma unroll
-                for (int o = 0; o < 12; ++o) zp[o] = 0.f;
-#pragma unroll
-                for (int i = 0; i < 2 * C; ++i) {
-                    const float4* zq = reinterpret_cast<const float4*>(&sm.zbuf[zs][i][0]);
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        const float4 f = zq[q];
-                        zp[4 * q] += f.x; zp[4 * q + 1] += f.y; zp[4 * q + 2] += f.z; zp[4 * q + 3] += f.w;
-                    }
-                }
-#pragma unroll
-                for (int o = 0; o < 12; ++o) z2[o] += zp[o];                // z2 = W2 h + b2 (Eq.2)
-                if constexpr (A2 == PNN_SOFTMAX) {
-                    // max and sum as trees (O = 10: depth 4 instead of 9)
-                    const float m = fmaxf(fmaxf(fmaxf(z2[0], z2[1]), fmaxf(z2[2], z2[3])),
-                                          fmaxf(fmaxf(fmaxf(z2[4], z2[5]), fmaxf(z2[6], z2[7])), fmaxf(z2[8], z2[9])));
-#pragma unroll
-                    for (int o = 0; o < O; ++o) dl[o] = __expf(z2[o] - m);
-                    const float sum = ((dl[0] + dl[1]) + (dl[2] + dl[3])) +
-                                      (((dl[4] + dl[5]) + (dl[6] + dl[7])) + (dl[8] + dl[9]));
-                    float inv;
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
-#pragma unroll
-                    for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == label) ? 1.f : 0.f);
-                    TR(10);
-                } else {
-                    // element-wise output (sigmoid / tanh, ½-SSE: Eq.9, R11): lane o forms output
-                    // o's activation and δ2 once, then every lane takes the ten by shuffles
-                    float zsel = z2[0];
-#pragma unroll
-                    for (int o = 1; o < O; ++o) zsel = (lane == o) ? z2[o] : zsel;
-                    const float x2 = act_fwd_t<A2>(zsel);
-                    const float dmine = (x2 - ((lane == label) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
-#pragma unroll
-                    for (int o = 0; o < O; ++o) dl[o] = __shfl_sync(0xffffffffu, dmine, o);
-                }
-            }
-            // ---- δ1, g(c) of unit uc; W2(c+1), b1(c+1), b2(c+1) ----
-            {
-                float s1 = 0.f;                    // (W2ᵀδ2)_u with the pre-update W2 (R6)
-#pragma unroll
-                for (int o = 0; o < O; ++o) s1 = fmaf(wv[o], dl[o], s1);
-                const float gu = lc ? lr * (s1 * act_deriv_t<A1>(h)) : 0.f;   // g(c) = η δ1
-                sm.gbuf[c % GR][uc] = gu;
-                TR(11);
-                sm.b1s[uc] -= gu;
-#pragma unroll
-                for (int o = 0; o < O; ++o) wv[o] = fmaf(-(lr * dl[o]), h, wv[o]);
-                float4* wq = reinterpret_cast<float4*>(&sm.w2s[uc][0]);
-                wq[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
-                wq[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
-                wq[2] = make_float4(wv[8], wv[9], 0.f, 0.f);
-            }
-            if (half == kB2Half && lane == 0) {        // b2(c+1) into the other buffer: the pair's
-                const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);   // partner may
-                float4* bq = reinterpret_cast<float4*>(&sm.b2s[(c + 1) & 1][0]);        // still read b2(c)
-                const float4 b0 = bo[0], b1v = bo[1], b2v = bo[2];
-                bq[0] = make_float4(fmaf(-lr, dl[0], b0.x), fmaf(-lr, dl[1], b0.y), fmaf(-lr, dl[2], b0.z),
-                                    fmaf(-lr, dl[3], b0.w));
-                bq[1] = make_float4(fmaf(-lr, dl[4], b1v.x), fmaf(-lr, dl[5], b1v.y), fmaf(-lr, dl[6], b1v.z),
-                                    fmaf(-lr, dl[7], b1v.w));
-                bq[2] = make_float4(fmaf(-lr, dl[8], b2v.x), fmaf(-lr, dl[9], b2v.y), 0.f, 0.f);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&sm.gready[c % GR]);
-                if (c + 1 < T) mbar_arrive(&sm.aready[(c + 1) % AR]);   // chain c+1 may start
-            }
-#if PNN_SWEEP_XWAIT
-            // off the critical path: every warp has passed U(c-1) (aready(c) above), so the
-            // slot of x(c-1-L) is free for x(c+PF); the sweeps wait for it themselves
-            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
-#endif
-            TR(6);
-        }
-        }
-        // U after the chains: a chain then starts right after its warps' F (warps 4-7, the
-        // sub-partition partners of 0-3, run U first: out of phase, 2 / 3 corrections)
-        if (!kStagger || warp < 4) u_pair(p);
-    }
-#else
-    int sx = 0;                                    // ring slot of x(s) = s % S
-    for (int s = 0; s <= T + LAG; ++s) {
-        TR(0);
-        // warps 4..7 (the sub-partition partners of warps 0..3) run U before F: the two sweeps
-        // of a sub-partition are then out of phase, and those rows' F(s) sees g(s-L) already
-        // applied (one correction term fewer in the chain)
-        if (warp < 4 || kV8SameOrder) {
-        if (s < T) {
-            // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
-#if PNN_SWEEP_XWAIT
-            mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));   // x(s) landed (usually long ago)
-#else
-            if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
-#endif
-            // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
-            const float* xn = xring + sx * DP + 4 * lane;
-            uint64_t acc[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = 0ull;
-            uint64_t xa, xb;
-            lds4(xn, xa, xb);
-#ifndef PNN_EXP_NO_SWEEP
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-#else
-            for (int q = 0; q < 0; ++q) {
-#endif
-                uint64_t na = 0ull, nb = 0ull;
-                if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);   // one quad ahead
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
-                    acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
-                }
-                xa = na;
-                xb = nb;
-            }
-            float px;                              // columns 768..783 of row tr
-            {
-                const float4 w4 = *reinterpret_cast<const float4*>(wxp);
-                const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
-                px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
-            }
-            float v[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                float lo, hi;
-                upk(acc[r], lo, hi);
-                v[r] = lo + hi;
-            }
-            // transpose-reduce 8 row sums over lanes 16/8/4: row (lane >> 2), part (lane & 3)
-            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-            float u4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
-            float u2[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-                u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
-            const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
-            sm.asum[s % AR][kr0 + tr][tq] = part;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
-        }
-            TR(1);
-        if (s >= LAG && s - LAG < T) {
-            // ---------------- U(s): W¹ -= g(s-L)·x(s-L)ᵀ ----------------
-            const int u = s - LAG;
-#ifndef PNN_EXP_NO_GWAIT
-            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
-#endif
-            const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
-            const float* xo = xring + su * DP + 4 * lane;
-            const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
-            const float4 g0 = gv[0], g1 = gv[1];
-            const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
-            uint64_t xa, xb;
-            lds4(xo, xa, xb);
-#ifndef PNN_EXP_NO_SWEEP
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-#else
-            for (int q = 0; q < 0; ++q) {
-#endif
-                uint64_t na = 0ull, nb = 0ull;
-                if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
-                    w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
-                }
-                xa = na;
-                xb = nb;
-            }
-            float4 w4 = *reinterpret_cast<const float4*>(wxp);
-            const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
-            const float gq = -sm.gbuf[u % GR][kr0 + tr];
-            w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
-            w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
-            *reinterpret_cast<float4*>(wxp) = w4;
-        }
-        } else {
-        if (s >= LAG && s - LAG < T) {
-            // ---------------- U(s): W¹ -= g(s-L)·x(s-L)ᵀ ----------------
-            const int u = s - LAG;
-#ifndef PNN_EXP_NO_GWAIT
-            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
-#endif
-            const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
-            const float* xo = xring + su * DP + 4 * lane;
-            const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
-            const float4 g0 = gv[0], g1 = gv[1];
-            const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
-            uint64_t xa, xb;
-            lds4(xo, xa, xb);
-#ifndef PNN_EXP_NO_SWEEP
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-#else
-            for (int q = 0; q < 0; ++q) {
-#endif
-                uint64_t na = 0ull, nb = 0ull;
-                if (q + 1 < NQ) lds4(xo + 128 * (q + 1), na, nb);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
-                    w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
-                }
-                xa = na;
-                xb = nb;
-            }
-            float4 w4 = *reinterpret_cast<const float4*>(wxp);
-            const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
-            const float gq = -sm.gbuf[u % GR][kr0 + tr];
-            w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
-            w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
-            *reinterpret_cast<float4*>(wxp) = w4;
-        }
-        if (s < T) {
-            // x(s) is certified by gready(s-1-LAG) (waited in U(s-1)); the first steps wait here
-#if PNN_SWEEP_XWAIT
-            mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));   // x(s) landed (usually long ago)
-#else
-            if (s <= LAG + 1) mbar_wait(&sm.xfull[s], 0u);
-#endif
-            // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
-            const float* xn = xring + sx * DP + 4 * lane;
-            uint64_t acc[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = 0ull;
-            uint64_t xa, xb;
-            lds4(xn, xa, xb);
-#ifndef PNN_EXP_NO_SWEEP
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-#else
-            for (int q = 0; q < 0; ++q) {
-#endif
-                uint64_t na = 0ull, nb = 0ull;
-                if (q + 1 < NQ) lds4(xn + 128 * (q + 1), na, nb);   // one quad ahead
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
-                    acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
-                }
-                xa = na;
-                xb = nb;
-            }
-            float px;                              // columns 768..783 of row tr
-            {
-                const float4 w4 = *reinterpret_cast<const float4*>(wxp);
-                const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
-                px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
-            }
-            float v[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                float lo, hi;
-                upk(acc[r], lo, hi);
-                v[r] = lo + hi;
-            }
-            // transpose-reduce 8 row sums over lanes 16/8/4: row (lane >> 2), part (lane & 3)
-            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-            float u4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
-            float u2[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-                u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
-            const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
-            sm.asum[s % AR][kr0 + tr][tq] = part;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
-        }
-            TR(1);
-        }
-        TR(2);
-
-        // ================= the chain of sample c = s - 1 (a pair of warps per sample) =================
-        const int c = s - 1;
-#ifdef PNN_EXP_NO_CHAIN
-        if (false) {
-#else
-        if (c >= 0 && c < T && (c % kChainPairs) + (4 - kChainPairs) == (warp >> 1)) {
-#endif
-            const int cs = (sx >= 1) ? sx - 1 : S - 1;          // ring slot of x(c)
-            // every warp's row sums of c and the end of chain c-1 (W2, b, g history in shared memory)
-            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
-            TR(3);
-            // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c); h(c) of unit uc ----
-            const float4 G = *reinterpret_cast<const float4*>(xring + cs * DP + GOFF);
-            const int label = __float_as_int(xring[cs * DP + GOFF + 4]);
-            const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][uc][0]);
-            float z = (pa.x + pa.y) + (pa.z + pa.w);
-            if (half == 0 || kV8SameOrder) z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);   // F-before-U rows
+            // the paired sweeps' F misses 4 updates (5 for odd samples)
+            if (c & 1) z = fmaf(-sm.gbuf[(c + GR - 5) % GR][uc], xring[cs * DP + GOFF + 5], z);
+            z = fmaf(-sm.gbuf[(c + GR - 4) % GR][uc], G.x, z);
             z = fmaf(-sm.gbuf[(c + GR - 3) % GR][uc], G.y, z);
             z = fmaf(-sm.gbuf[(c + GR - 2) % GR][uc], G.z, z);
             z = fmaf(-sm.gbuf[(c + GR - 1) % GR][uc], G.w, z);
@@ -921,13 +513,6 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
             // ---- while the exchange is in flight: certify x(c+2+L) for the sweeps' F(c+2+L),
             //      which comes after their wait on gready(c) (first warp of the pair) ----
             // every warp has passed U(c-1) (aready(c) above): the slot of x(c-1-L) is free for x(c+PF)
-#if !PNN_SWEEP_XWAIT
-            if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
-            if (half == 0 && c + 2 + LAG < T) {
-                const int u = c + 2 + LAG;
-                mbar_wait(&sm.xfull[(cs + 2 + LAG) % S], (uint32_t)((u / S) & 1));
-            }
-#endif
             TR(4);
             // ---- δ2(c) in every lane: z2 = Σ partials + b2(c) ----
             mbar_wait(&sm.zfull[zs], (uint32_t)((c / ZS) & 1));
@@ -1013,16 +598,15 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
                 mbar_arrive(&sm.gready[c % GR]);
                 if (c + 1 < T) mbar_arrive(&sm.aready[(c + 1) % AR]);   // chain c+1 may start
             }
-#if PNN_SWEEP_XWAIT
             // off the critical path: every warp has passed U(c-1) (aready(c) above), so the
             // slot of x(c-1-L) is free for x(c+PF); the sweeps wait for it themselves
             if (half == 0 && lane == 0 && c + PF < T) issue_x(c + PF, (cs + PF) % S);
-#endif
             TR(6);
         }
-        if (++sx == S) sx = 0;
+        }
+        // U after the chains: a chain then starts right after its warps' F
+        u_pair(p);
     }
-#endif
 #undef TR
 
     // ---- write back ----
@@ -1063,18 +647,8 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
 // g(c) of each unit back to the owning sweep CTA (st.async → that CTA's gready).  The
 // chain never shares an SM sub-partition with a sweep, and the sweeps never run chain
 // code, so the period is max(sweep, chain) instead of their contended sum.
-#ifndef PNN_SPLIT_SAME_ORDER
-#define PNN_SPLIT_SAME_ORDER 0
-#endif
-// every sweep warp runs F then U (one code stream per SM sub-partition) instead of the
-// v8 phase shift (warps 4..7: U then F)
-constexpr bool kSplitSameOrder = PNN_SPLIT_SAME_ORDER != 0;
-// paired sweeps (as v8's PNN_V8_PAIRS): F / U for two samples per pass, one complete row sum
-// per unit sent to the chain CTA, 5 Gram corrections for odd samples
-#ifndef PNN_SPLIT_PAIRS
-#define PNN_SPLIT_PAIRS 1
-#endif
-constexpr bool kSplitPairs = PNN_SPLIT_PAIRS != 0;
+// paired sweeps (as v8's): F / U for two samples per pass, one complete row sum per unit
+// sent to the chain CTA, 5 Gram corrections for odd samples
 constexpr int RS = 16;               // chain CTA: Gram-record ring slots
 constexpr int RPF = 8;               // records in flight
 constexpr int SPF = S - 2 * LAG - 1; // sweep CTAs: x prefetch distance (slot provably free, see below)
@@ -1171,94 +745,6 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
         const uint32_t abar = mapa(smem_u32(&sm.aready[0]), (uint32_t)NSW);
         constexpr uint32_t kAStride = 2 * UMAX * 4 * 4;
 
-        auto sweep_f = [&](int s, int sx) {
-            mbar_wait(&sm.xfull[sx], (uint32_t)((s / S) & 1));
-            const float* xn = xring + sx * DP + 4 * lane;
-            uint64_t acc[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = 0ull;
-            uint64_t xa, xb, ya, yb;                  // x quads q and q+1 in flight (2 ahead)
-            lds4(xn, xa, xb);
-            lds4(xn + 128, ya, yb);
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                uint64_t na = 0ull, nb = 0ull;
-                if (q + 2 < NQ) lds4(xn + 128 * (q + 2), na, nb);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
-                    acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
-                }
-                xa = ya; xb = yb;
-                ya = na; yb = nb;
-            }
-            float px;
-            {
-                const float4 w4 = *reinterpret_cast<const float4*>(wxp);
-                const float4 x4 = *reinterpret_cast<const float4*>(xring + sx * DP + XC + 4 * tq);
-                px = fmaf(w4.w, x4.w, fmaf(w4.z, x4.z, fmaf(w4.y, x4.y, w4.x * x4.x)));
-            }
-            float v[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                float lo, hi;
-                upk(acc[r], lo, hi);
-                v[r] = lo + hi;
-            }
-            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-            float u4[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
-            float u2[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-                u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
-            const float part = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4) + px;
-            const int a = s % AR;
-            st_async_f32_if(xlive, apart + (uint32_t)a * kAStride, part, abar + (uint32_t)a * 8u);
-        };
-#ifdef PNN_SPLIT_PROFILE
-        long long pw_g = 0, pw_tot0 = ptx::clock64();
-#endif
-        auto sweep_u = [&](int s, int sx) {
-            const int u = s - LAG;
-#ifdef PNN_SPLIT_PROFILE
-            const long long t0 = ptx::clock64();
-#endif
-            mbar_wait(&sm.gready[u % GR], (uint32_t)((u / GR) & 1));
-#ifdef PNN_SPLIT_PROFILE
-            pw_g += ptx::clock64() - t0;
-#endif
-            const int su = (sx >= LAG) ? sx - LAG : sx + S - LAG;
-            const float* xo = xring + su * DP + 4 * lane;
-            const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[u % GR][kr0]);
-            const float4 g0 = gv[0], g1 = gv[1];
-            const float gp[R] = {-g0.x, -g0.y, -g0.z, -g0.w, -g1.x, -g1.y, -g1.z, -g1.w};
-            uint64_t xa, xb, ya, yb;
-            lds4(xo, xa, xb);
-            lds4(xo + 128, ya, yb);
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                uint64_t na = 0ull, nb = 0ull;
-                if (q + 2 < NQ) lds4(xo + 128 * (q + 2), na, nb);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    w[r][2 * q] = ffma2(pk(gp[r], gp[r]), xa, w[r][2 * q]);
-                    w[r][2 * q + 1] = ffma2(pk(gp[r], gp[r]), xb, w[r][2 * q + 1]);
-                }
-                xa = ya; xb = yb;
-                ya = na; yb = nb;
-            }
-            float4 w4 = *reinterpret_cast<const float4*>(wxp);
-            const float4 x4 = *reinterpret_cast<const float4*>(xring + su * DP + XC + 4 * tq);
-            const float gq = -sm.gbuf[u % GR][kr0 + tr];
-            w4.x = fmaf(gq, x4.x, w4.x); w4.y = fmaf(gq, x4.y, w4.y);
-            w4.z = fmaf(gq, x4.z, w4.z); w4.w = fmaf(gq, x4.w, w4.w);
-            *reinterpret_cast<float4*>(wxp) = w4;
-        };
-
-        if constexpr (kSplitPairs) {
         const int trow = lane >> 2, tsmp = (lane >> 1) & 1, th8 = lane & 1;
         const bool rlive = kr0 + trow < Uown;
         const uint32_t apart0 = mapa(smem_u32(&sm.asum[0][k0 + kr0 + trow][0]), (uint32_t)NSW);
@@ -1387,31 +873,6 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
                 if (s0 + 1 + SPF < T) issue_x(s0 + 1 + SPF);
             }
         }
-        } else {
-        int sx = 0;                                // ring slot of x(s)
-        for (int s = 0; s < T + LAG; ++s) {
-            // g(s) of this CTA's rows will arrive from the chain CTA: post the expected bytes
-            if (threadIdx.x == 0 && s < T) mbar_arrive_expect_tx(&sm.gready[s % GR], 4u * (uint32_t)Uown);
-            const bool do_f = s < T, do_u = s >= LAG && s - LAG < T;
-            if (warp < 4 || kSplitSameOrder) {     // F before U (L correction terms in the chain)
-                if (do_f) sweep_f(s, sx);
-                if (do_u) sweep_u(s, sx);
-                // x(s+SPF) goes to the slot of x(s-2L-1), last read by U(s-L-1); every warp
-                // finished it before its F(s-L) parts reached the chain, i.e. before gready(s-L)
-                // (waited in U(s) just above) could complete
-                if (threadIdx.x == 0 && s + SPF < T) issue_x(s + SPF);   // (warp 0: F, U order)
-            } else {                               // U before F (one term fewer)
-                if (do_u) sweep_u(s, sx);
-                if (do_f) sweep_f(s, sx);
-            }
-            if (++sx == S) sx = 0;
-        }
-        }
-#ifdef PNN_SPLIT_PROFILE
-        if (blockIdx.x == 0 && lane == 0)
-            printf("sweep cta0 warp %d: T %d total %lld cyc/sample, gready wait %lld cyc/sample\n", warp, T,
-                   (ptx::clock64() - pw_tot0) / T, pw_g / T);
-#endif
         float* W1o = opaque(W1);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -1435,7 +896,6 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
         const bool lc = u < H;
         const int sr = lc ? u / U : 0;             // owning sweep CTA and its row
         const int r = u - sr * U;
-        const bool four = kSplitPairs || kSplitSameOrder || r < 32;   // rows of warps running F before U
         float w2[O], b2[O];
 #pragma unroll
         for (int o = 0; o < O; ++o) {
@@ -1454,29 +914,20 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
         };
         if (threadIdx.x == 0)
             for (int c = 0; c < RPF && c < T; ++c) issue_rec(c);
-#ifdef PNN_SPLIT_PROFILE
-        long long pc_a = 0, pc_tot0 = ptx::clock64(), pc_tmp = 0;
-#endif
         for (int c = 0; c < T; ++c) {
             if (threadIdx.x == 0) {
-                mbar_arrive_expect_tx(&sm.aready[c % AR], (kSplitPairs ? 4u : 16u) * (uint32_t)H);   // parts of every unit
+                mbar_arrive_expect_tx(&sm.aready[c % AR], 4u * (uint32_t)H);   // parts of every unit
                 if (c + RPF < T) issue_rec(c + RPF);      // its slot held rec(c+RPF-RS): consumed
             }
             mbar_wait(&sm.rfull[c % RS], (uint32_t)((c / RS) & 1));
             const float4 G = sm.rec[c % RS][0];
             const int label = __float_as_int(sm.rec[c % RS][1].x);
-#ifdef PNN_SPLIT_PROFILE
-            pc_tmp = ptx::clock64();
-#endif
             mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
-#ifdef PNN_SPLIT_PROFILE
-            pc_a += ptx::clock64() - pc_tmp;
-#endif
             // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c) (R27), h(c) ----
             const float4 pa = *reinterpret_cast<const float4*>(&sm.asum[c % AR][u][0]);
-            float z = kSplitPairs ? pa.x : (pa.x + pa.y) + (pa.z + pa.w);
-            if (kSplitPairs && (c & 1)) z = fmaf(-g5, sm.rec[c % RS][1].y, z);
-            if (four) z = fmaf(-g4, G.x, z);
+            float z = pa.x;
+            if (c & 1) z = fmaf(-g5, sm.rec[c % RS][1].y, z);
+            z = fmaf(-g4, G.x, z);
             z = fmaf(-g3, G.y, z);
             z = fmaf(-g2, G.z, z);
             z = fmaf(-g1, G.w, z);
@@ -1555,11 +1006,6 @@ sgd_split_kernel(NetDesc d, float* __restrict__ children, const float* __restric
             }
             g5 = g4; g4 = g3; g3 = g2; g2 = g1; g1 = gu;
         }
-#ifdef PNN_SPLIT_PROFILE
-        if (blockIdx.x == NSW && lane == 0)
-            printf("chain warp %d: T %d total %lld cyc/sample, aready wait %lld cyc/sample\n", warp, T,
-                   (ptx::clock64() - pc_tot0) / T, pc_a / T);
-#endif
         if (lc) {
 #pragma unroll
             for (int o = 0; o < O; ++o) opaque(W2)[(long long)o * H + u] = w2[o];
