@@ -605,7 +605,9 @@ sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __rest
         }
         }
         // U after the chains: a chain then starts right after its warps' F
+        TR(12);
         u_pair(p);
+        TR(2);
     }
 #undef TR
 
