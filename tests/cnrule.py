@@ -11,7 +11,7 @@ of the fp32 oracle.  A CN over that bar passes only with a recorded cause:
     (R22, tests/envelope.py): no larger than the oracle's own spread under 1-ulp
     perturbations of its inputs (64 trials: a further valid trajectory lands outside with
     probability ~1/65) or the spread of another valid fp32
-    ordering (torch, per-sample SGD only).
+    ordering (torch: BLAS summation order, per-sample or mini-batch).
 The merged net is the mean of the children, so its bound is the mean of their bounds.
 """
 from __future__ import annotations
@@ -42,8 +42,8 @@ def cn_bound(orc, net, layers, act, init, lr, Xi, yi, err, okid, epochs, batch=1
         # no kink: a gradual divergence — the slice is ill-conditioned in fp32 (R22, as C2)
     from tests.envelope import perturbation_envelope, torch_sgd_fp32
     env = perturbation_envelope(orc, layers, act, p0, Xi, yi, lr, epochs, batch=batch)
-    if batch == 1:
-        env = max(env, float(np.abs(torch_sgd_fp32(layers, act, p0, Xi, yi, lr, epochs) - okid).max()))
+    if all(a in ("sigmoid", "tanh", "relu", "softmax") for a in act):
+        env = max(env, float(np.abs(torch_sgd_fp32(layers, act, p0, Xi, yi, lr, epochs, batch) - okid).max()))
     info["envelope"] = env
     return max(TOL, env), info
 

@@ -21,7 +21,9 @@ import numpy as np
 import torch
 
 
-def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1):
+def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1, batch=1):
+    """The paper's SGD (batch 1) or mini-batch GD (batch > 1: per-instance gradients summed
+    by a BLAS matmul over the batch, averaged over its size, R14) in torch CPU fp32."""
     torch.set_num_threads(1)
     W, b, off = [], [], 0
     for l in range(1, len(layers)):
@@ -35,12 +37,13 @@ def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1):
     f = {"sigmoid": torch.sigmoid, "tanh": torch.tanh, "relu": torch.relu}
     L = len(layers) - 1
     for _ in range(epochs):
-        for t in range(len(y)):
-            xs = [Xt[t]]
+        for t0 in range(0, len(y), batch):
+            xs = [Xt[t0:t0 + batch]]                     # rows = instances of the batch
             for l in range(L):
-                z = W[l] @ xs[-1] + b[l]
-                xs.append(torch.softmax(z, 0) if act[l] == "softmax" else f[act[l]](z))
-            o, e = xs[-1], eye[int(y[t])]
+                z = xs[-1] @ W[l].T + b[l]
+                xs.append(torch.softmax(z, 1) if act[l] == "softmax" else f[act[l]](z))
+            o = xs[-1]
+            e = eye[torch.as_tensor(np.asarray(y[t0:t0 + batch], np.int64))]
             if act[-1] == "softmax":
                 d = o - e
             elif act[-1] == "sigmoid":
@@ -53,11 +56,16 @@ def torch_sgd_fp32(layers, act, params, X, y, lr, epochs=1):
             for l in range(L - 1, 0, -1):
                 a = xs[l]
                 g = {"sigmoid": a * (1 - a), "tanh": 1 - a * a, "relu": (a > 0).float()}[act[l - 1]]
-                ds.insert(0, (W[l].T @ ds[0]) * g)
+                ds.insert(0, (ds[0] @ W[l]) * g)
+            bsz = xs[0].shape[0]
             for l in range(L):
-                gl = lr * ds[l]
-                W[l] -= torch.outer(gl, xs[l])
-                b[l] -= gl
+                if bsz == 1:
+                    gl = lr * ds[l][0]
+                    W[l] -= torch.outer(gl, xs[l][0])
+                    b[l] -= gl
+                else:
+                    W[l] -= lr * ((ds[l].T @ xs[l]) / bsz)
+                    b[l] -= lr * (ds[l].sum(0) / bsz)
     return np.concatenate([np.concatenate([W[l].ravel().numpy(), b[l].numpy()]) for l in range(L)])
 
 

@@ -380,3 +380,18 @@ def test_fp32_ordering_envelope():
     X1, y1 = make_split(1000, "train", 0)
     assert perturbation_envelope(oracle, c1.layers, c1.act, oracle.init_params(c1.layers, c1.init, 0),
                                  X1, y1, c1.lr, trials=1) < 1e-5
+
+
+def test_fp32_ordering_envelope_minibatch():
+    """The mini-batch arm of tests/envelope.py (batch gradient as one BLAS matmul,
+    averaged over the batch, R14 short last batch) agrees with the fp32 oracle's
+    mini-batch GD to 1e-6 on a well-conditioned tanh net with a ragged last batch; a
+    transposed or unscaled batch gradient would miss by orders of magnitude."""
+    import oracle
+    X, y = make_split(203, "train", 0)
+    layers, act = [784, 32, 10], ["tanh", "softmax"]
+    p0 = oracle.init_params(layers, "xavier", 0)
+    from tests.envelope import torch_sgd_fp32
+    d = np.abs(torch_sgd_fp32(layers, act, p0, X, y, 0.05, 2, batch=7)
+               - oracle.train(layers, act, p0, X, y, 0.05, 2, batch=7))
+    assert d.max() < 1e-6
