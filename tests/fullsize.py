@@ -91,7 +91,7 @@ def run_full(orc, name, epochs=None, threads=None, variant=None, log=print):
                 a, b = int(start[i]), int(start[i] + count[i])
                 from tests.cnrule import cn_bound
                 bound, info = cn_bound(orc, net, c.layers, c.act, c.init, c.lr, X[a:b], y[a:b], err, okids[i], E,
-                                       c.batch)
+                                       c.batch, kid=kids[i])
                 cn.update(info or {})
             cn["bound"] = bound
             cn["ok"] = err < TOL or err <= bound

@@ -77,7 +77,7 @@ def test_short_and_ragged_slices(orc, rows_per_cn):
 def test_f1_full_sampled(orc):
     """F1 at its full size (60,000 rows, K = 10, 20 epochs, batch 50; the configuration
     bench.py times) on the resident mini-batch kernel; the oracle re-trains CNs 0 and 9.
-    Per-CN rule of tests/cnrule.py (ReLU: a logged kink, R24)."""
+    Per-CN rule of tests/cnrule.py (ReLU: a logged kink, R24; the envelope, R22; R34)."""
     from paper_2304_09590_b200 import PNN
     c = CONFIGS["F1"]
     X, y = make_split(c.n_train, "train", 0)
@@ -95,10 +95,11 @@ def test_f1_full_sampled(orc):
     from tests.cnrule import cn_bound
     report = []
     for j, i in enumerate(sample):
-        err = float(np.abs(net.get_params(i) - okids[j]).max())
+        kid = net.get_params(i)
+        err = float(np.abs(kid - okids[j]).max())
         a, b = int(start[i]), int(start[i] + count[i])
         bound, info = cn_bound(orc, net, c.layers, c.act, c.init, c.lr, X[a:b], y[a:b], err, okids[j], c.epochs,
-                               c.batch)
+                               c.batch, kid=kid)
         report.append((i, err, bound, info))
         assert err < TOL or err <= bound, f"CN {i}: max-abs {err:.3g} without a recorded cause: {info}"
     print("F1 full per-CN (index, max-abs, bound, cause):", report)

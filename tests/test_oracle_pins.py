@@ -395,3 +395,21 @@ def test_fp32_ordering_envelope_minibatch():
     d = np.abs(torch_sgd_fp32(layers, act, p0, X, y, 0.05, 2, batch=7)
                - oracle.train(layers, act, p0, X, y, 0.05, 2, batch=7))
     assert d.max() < 1e-6
+
+
+def test_r34_rejects_an_inaccurate_result():
+    """R34 (tests/cnrule.py) passes a CN beyond the fp32 envelope only if the GPU is no
+    farther from the fp64 run of the same algorithm than the fp32 oracle is: a result off
+    by 2e-3 in one weight is rejected, the fp32 oracle's own result is accepted."""
+    import oracle
+    from tests.cnrule import cn_bound
+    X, y = make_split(120, "train", 0)
+    layers, act = [784, 32, 10], ["sigmoid", "sigmoid"]
+    p0 = oracle.init_params(layers, "uniform", 0)
+    okid = oracle.train(layers, act, p0, X, y, 0.1)
+    bad = okid.copy()
+    bad[5] += 2e-3
+    bound, info = cn_bound(oracle, None, layers, act, "uniform", 0.1, X, y, 2e-3, okid, 1, kid=bad)
+    assert bound < 2e-3 and info["fp64"]["gpu_vs_fp64"] > info["fp64"]["oracle32_vs_fp64"]
+    bound, info = cn_bound(oracle, None, layers, act, "uniform", 0.1, X, y, 2e-3, okid, 1, kid=okid)
+    assert bound == 2e-3
