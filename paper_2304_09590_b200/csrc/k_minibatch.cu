@@ -10,6 +10,8 @@
 #include "pnn_internal.h"
 #include "k_tcgemm.cuh"
 
+extern long long* g_trace;   // debug timeline (k_resident.cu; tools/trace_tc.py)
+
 namespace {
 
 using PFN_encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -44,6 +46,26 @@ bool make_tmap_kmajor(CUtensorMap* tm, const void* base, int K, int rows, int Z,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel may start while the
+// previous kernel of the stream finishes; it runs its prologue (barrier init, TMEM
+// allocation, tensor-map prefetch) and then waits in griddep_wait() for that kernel's
+// completion.  Inside the epoch's CUDA graph this becomes a programmatic edge.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int BN, int EPI>
 static cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int Z, int M, int N, int K,
                                const tc::Epi& ep, cudaStream_t st) {
@@ -60,8 +82,7 @@ static cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int
         }
     }
     dim3 grid((unsigned)((M + tc::BM - 1) / tc::BM), (unsigned)((N + BN - 1) / BN), (unsigned)Z);
-    kern<<<grid, tc::threads_for(BN), smem, st>>>(ta, tb, K, ep);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, dim3(tc::threads_for(BN)), smem, st, ta, tb, K, ep);
 }
 
 // Test hook (tests/test_gpu_tcgemm.py): C[z][m][n] = Σ_k A[z][m][k]·B[z][n][k], fp32 out.
@@ -70,6 +91,7 @@ extern "C" int pnn_debug_tc_gemm(const void* A, const void* B, float* C, int Z, 
     if (!make_tmap_kmajor(&ta, A, K, M, Z, tc::BM)) return 1;
     if (!make_tmap_kmajor(&tb, B, K, N, Z, bn)) return 2;
     tc::Epi ep{};
+    ep.trace = g_trace;
     ep.M = M;
     ep.N = N;
     ep.nvalid = N;
@@ -279,13 +301,21 @@ __global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, Mb
     long long st;
     const long long cnt = slice_rows(n_local, K_local, z, &st);
     const int w = (s.D - d0) < 64 ? (s.D - d0) : 64;
-    for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
-        const int b = idx >> 6, dd = idx & 63;
+    // all 16 loads of a thread are issued before any store (one memory round trip, not 16)
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int idx = threadIdx.x + 256 * i, b = idx >> 6, dd = idx & 63;
         const long long tr = (long long)step * s.B + b;
+        v[i] = (b < s.B && dd < w && tr < cnt) ? X[(st + tr) * s.D + d0 + dd] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int idx = threadIdx.x + 256 * i, b = idx >> 6, dd = idx & 63;
         if (b < s.B && dd < w) {
-            const __nv_bfloat16 v = __float2bfloat16_rn(tr < cnt ? X[(st + tr) * s.D + d0 + dd] : 0.f);
-            xs[((long long)z * s.B + b) * s.D + d0 + dd] = v;
-            t[b][dd] = v;
+            const __nv_bfloat16 h = __float2bfloat16_rn(v[i]);
+            xs[((long long)z * s.B + b) * s.D + d0 + dd] = h;
+            t[b][dd] = h;
         }
     }
     __syncthreads();
@@ -295,32 +325,57 @@ __global__ void __launch_bounds__(256) mb_cast_x(const float* __restrict__ X, Mb
     }
 }
 
-// Output layer backward (grid: H2/64 × CNs, 256 threads = 64 hidden units × 4 batch
-// quarters): dW3 = δ3bᵀ·A2 → W3, W3b; dA2 = δ3b·W3b (pre-update W3, R6); δ2 = dA2 ⊙
+// Output layer backward (grid: H2/64 × CNs, 512 threads = 64 hidden units × 8 batch
+// eighths): dW3 = δ3bᵀ·A2 → W3, W3b; dA2 = δ3b·W3b (pre-update W3, R6); δ2 = dA2 ⊙
 // [A2 > 0] (R9) → δ2b [B][H2] and δ2bT [H2][B]; b2 -= η·Σδ2/B; block 0 also b3 -= η·Σδ3/B.
-__global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, const int32_t* __restrict__ Y,
+__global__ void __launch_bounds__(512) mb_out_bwd(float* __restrict__ children, const int32_t* __restrict__ Y,
                                                   MbState s, long long n_local, int K_local, int z0, int step,
-                                                  float lr) {
-    __shared__ float d3s[64][16];                  // δ3b (bf16-rounded) of the batch
+                                                  float lr, long long* trace) {
+    // debug timeline (nullable; tools/trace_tc.py): per CTA [0] %globaltimer at entry, clock64 at
+    // [1] entry, [2] after griddep_wait, [3] δ3 ready, [4] end
+    long long* trc = (trace && threadIdx.x == 0) ? trace + 24LL * (blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
+    auto tstamp = [&](int i) {
+        if (trc) {
+            long long t;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+            trc[i] = t;
+        }
+    };
+    if (trc) {
+        long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        trc[0] = g;
+        tstamp(1);
+    }
+    __shared__ __align__(16) float d3s[64][16];    // δ3b (bf16-rounded) of the batch
     __shared__ float d3f[64][16];                  // δ3 in fp32 (the b3 update)
-    __shared__ float part[3][64][17];
+    __shared__ float part[7][64][17];
     const int z = z0 + blockIdx.y;
+    ptx::griddep_wait();                           // PDL: F2's outputs are complete
+    ptx::griddep_launch();
+    tstamp(2);
     long long st;
     const long long cnt = slice_rows(n_local, K_local, z, &st);
     long long bsz = cnt - (long long)step * s.B;
     bsz = bsz < 0 ? 0 : (bsz > s.B ? s.B : bsz);
     const float scale = bsz > 0 ? lr / (float)bsz : 0.f;
     float* P = children + (long long)z * s.P;
-    // ---- output layer forward from F2's fused partials: z3 = Σ_tiles + b3, softmax (R4),
-    //      δ3 = p − e (Eq.10; 0 past the batch); every CTA of the CN computes all rows ----
+    const int jl = threadIdx.x & 63, g = threadIdx.x >> 6;   // unit j, batch eighth g (rows 8g..8g+7)
+    const int j = blockIdx.x * 64 + jl;
+    // every global operand is loaded up front (the step is latency-bound): first the δ3
+    // inputs of the 64 threads that form the softmax (the critical chain), then the rest
+    const int nt = s.H2 / tc::BM;
+    float zz[16], bb[16];
+    int label = -1;
     if (threadIdx.x < 64) {
         const int b = threadIdx.x;
         const float* b3 = P + s.woff3 + (long long)s.O * s.H2;
-        const int nt = s.H2 / tc::BM;
-        float zz[16];
+        label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;
 #pragma unroll
-        for (int o = 0; o < 16; ++o) zz[o] = 0.f;
-        const int label = (b < bsz) ? Y[st + (long long)step * s.B + b] : -1;   // issued early
+        for (int o = 0; o < 16; ++o) {
+            zz[o] = 0.f;
+            bb[o] = (o < s.O) ? b3[o] : 0.f;
+        }
 #pragma unroll 8
         for (int t = 0; t < nt; ++t) {                 // (the tiles' loads issue together)
             const float4* zq = reinterpret_cast<const float4*>(s.z3part + (((long long)z * nt + t) * 64 + b) * 16);
@@ -330,10 +385,32 @@ __global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, 
                 zz[4 * q] += f.x; zz[4 * q + 1] += f.y; zz[4 * q + 2] += f.z; zz[4 * q + 3] += f.w;
             }
         }
+    }
+    __nv_bfloat16* w3b = s.W3b + (long long)z * 16 * s.H2;
+    float wold[16], a[8], w3m[16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o) wold[o] = (o < s.O) ? __bfloat162float(w3b[(long long)o * s.H2 + j]) : 0.f;
+    const __nv_bfloat16* a2 = s.A2 + (long long)z * s.B * s.H2 + j;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = __bfloat162float(a2[(long long)(8 * g + q) * s.H2]);
+    float* W3 = P + s.woff3;
+    float b2old = 0.f;
+    if (g == 0) {
+#pragma unroll
+        for (int o = 0; o < 16; ++o) w3m[o] = (o < s.O) ? W3[(long long)o * s.H2 + j] : 0.f;
+        b2old = P[s.woff2 + (long long)s.H2 * s.H1 + j];
+    }
+    tstamp(5);
+    // ---- output layer forward from F2's fused partials: z3 = Σ_tiles + b3, softmax (R4),
+    //      δ3 = p − e (Eq.10; 0 past the batch and for o ≥ O); every CTA of the CN computes all rows ----
+    if (threadIdx.x < 64) {
+        const int b = threadIdx.x;
         float m = -INFINITY;
 #pragma unroll
         for (int o = 0; o < 16; ++o)
-            if (o < s.O) { zz[o] = b3[o] + zz[o]; m = fmaxf(m, zz[o]); }
+            if (o < s.O) { zz[o] = bb[o] + zz[o]; m = fmaxf(m, zz[o]); }
+        if (m == 12345.f) tstamp(9);               // (never: keeps the next stamp after the sums)
+        tstamp(6);
         float sum = 0.f;
 #pragma unroll
         for (int o = 0; o < 16; ++o)
@@ -348,48 +425,45 @@ __global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, 
             d3f[b][o] = dl;
             d3s[b][o] = __bfloat162float(__float2bfloat16_rn(dl));
         }
+        tstamp(7);
     }
     __syncthreads();
+    tstamp(3);
     if (blockIdx.x == 0 && threadIdx.x < s.O) {        // b3 -= η·(Σ_b δ3 / B), δ3 in fp32
         float t = 0.f;
         for (int b = 0; b < s.B; ++b) t += d3f[b][threadIdx.x];
         P[s.woff3 + (long long)s.O * s.H2 + threadIdx.x] -= scale * t;
     }
-    const int jl = threadIdx.x & 63, g = threadIdx.x >> 6;
-    const int j = blockIdx.x * 64 + jl;
-    __nv_bfloat16* w3b = s.W3b + (long long)z * 16 * s.H2;
-    float wold[16], gw[16];
+    // dW3 partial (this eighth's rows) and δ2 = (δ3b·W3b) ⊙ [A2 > 0]; δ3b rows read as float4
+    // (entries o ≥ O are 0, and so are wold[o ≥ O])
+    float gw[16];
 #pragma unroll
-    for (int o = 0; o < 16; ++o) {
-        wold[o] = (o < s.O) ? __bfloat162float(w3b[(long long)o * s.H2 + j]) : 0.f;
-        gw[o] = 0.f;
-    }
+    for (int o = 0; o < 16; ++o) gw[o] = 0.f;
     float db = 0.f;
-    const __nv_bfloat16* a2 = s.A2 + (long long)z * s.B * s.H2 + j;
     __nv_bfloat16* d2b = s.d2b + (long long)z * s.B * s.H2 + j;
-    uint4* d2bT = reinterpret_cast<uint4*>(s.d2bT + ((long long)z * s.H2 + j) * s.B + 16 * g);
+    __align__(16) __nv_bfloat16 pk[8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        __align__(16) __nv_bfloat16 pk[8];
+    for (int q = 0; q < 8; ++q) {
+        const int b = 8 * g + q;
+        const float av = a[q];
+        const float4* dq = reinterpret_cast<const float4*>(&d3s[b][0]);
+        float da = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int b = 16 * g + 8 * h + q;
-            const float a = __bfloat162float(a2[(long long)b * s.H2]);
-            float da = 0.f;
+        for (int u = 0; u < 4; ++u) {
+            const float4 d4 = dq[u];
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-            for (int o = 0; o < 16; ++o) {
-                if (o < s.O) {
-                    gw[o] = fmaf(d3s[b][o], a, gw[o]);
-                    da = fmaf(wold[o], d3s[b][o], da);
-                }
+            for (int k = 0; k < 4; ++k) {
+                gw[4 * u + k] = fmaf(dv[k], av, gw[4 * u + k]);
+                da = fmaf(wold[4 * u + k], dv[k], da);
             }
-            const float d2 = (a > 0.f) ? da : 0.f;
-            pk[q] = __float2bfloat16_rn(d2);
-            d2b[(long long)b * s.H2] = pk[q];
-            db += d2;
         }
-        d2bT[h] = *reinterpret_cast<const uint4*>(pk);
+        const float d2 = (av > 0.f) ? da : 0.f;
+        pk[q] = __float2bfloat16_rn(d2);
+        d2b[(long long)b * s.H2] = pk[q];
+        db += d2;
     }
+    *reinterpret_cast<uint4*>(s.d2bT + ((long long)z * s.H2 + j) * s.B + 8 * g) = *reinterpret_cast<const uint4*>(pk);
     if (g > 0) {
 #pragma unroll
         for (int o = 0; o < 16; ++o) part[g - 1][jl][o] = gw[o];
@@ -397,22 +471,22 @@ __global__ void __launch_bounds__(256) mb_out_bwd(float* __restrict__ children, 
     }
     __syncthreads();
     if (g == 0) {
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 7; ++q) {
 #pragma unroll
             for (int o = 0; o < 16; ++o) gw[o] += part[q][jl][o];
             db += part[q][jl][16];
         }
-        float* W3 = P + s.woff3;
 #pragma unroll
         for (int o = 0; o < 16; ++o) {
             if (o < s.O) {
-                const float w = fmaf(-scale, gw[o], W3[(long long)o * s.H2 + j]);
+                const float w = fmaf(-scale, gw[o], w3m[o]);
                 W3[(long long)o * s.H2 + j] = w;
                 w3b[(long long)o * s.H2 + j] = __float2bfloat16_rn(w);
             }
         }
-        P[s.woff2 + (long long)s.H2 * s.H1 + j] -= scale * db;
+        P[s.woff2 + (long long)s.H2 * s.H1 + j] = b2old - scale * db;
     }
+    tstamp(4);
 }
 
 }  // namespace
@@ -446,6 +520,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         }
         // F1: A1 = relu(W1b·Xsᵀ + b1)
         tc::Epi f1 = base;
+        f1.trace = g_trace ? g_trace + 1 * 16384LL : nullptr;
         f1.M = s->H1; f1.N = B; f1.nvalid = B;
         f1.bias = children + s->woff1 + (long long)s->H1 * s->D; f1.zs_bias = s->P;
         f1.out_bm = s->A1; f1.out_mb = s->A1T; f1.zs_act = (long long)s->H1 * B;
@@ -462,18 +537,22 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         }
         // F2: A2 = relu(W2b·A1ᵀ + b2)
         tc::Epi f2 = base;
+        f2.trace = g_trace ? g_trace + 2 * 16384LL : nullptr;
         f2.M = s->H2; f2.N = B; f2.nvalid = B;
         f2.bias = children + s->woff2 + (long long)s->H2 * s->H1; f2.zs_bias = s->P;
         f2.out_bm = s->A2; f2.out_mb = nullptr; f2.zs_act = (long long)s->H2 * B;
         f2.w3 = s->W3b; f2.z3part = s->z3part;          // the output layer's partials, fused
         if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW2b, s->tA1, s_count, s->H2, B, s->H1, f2, st))) return e;
         // output layer (CUDA cores: N = 10 / K = 10 are not dense contractions)
-        mb_out_bwd<<<dim3((unsigned)(s->H2 / 64), (unsigned)s_count), 256, 0, st>>>(
-            children, y, *s, n_local, K_local, s_first, (int)j, lr);
+        if ((e = launch_pdl(mb_out_bwd, dim3((unsigned)(s->H2 / 64), (unsigned)s_count), dim3(512), 0, st,
+                            children, y, *s, n_local, K_local, s_first, (int)j, lr,
+                            g_trace ? g_trace + 6 * 16384LL : (long long*)nullptr)))
+            return e;
         if ((e = cudaEventRecord(s->ev_ob, st))) return e;
         const bool odd = (j & 1) != 0;
         // B4: δ1 = (W2bᵀ·δ2b) ⊙ [A1 > 0]; b1 update (pre-update W2: before B3)
         tc::Epi b4 = base;
+        b4.trace = g_trace ? g_trace + 3 * 16384LL : nullptr;
         b4.M = s->H1; b4.N = B; b4.nvalid = B;
         b4.mask = s->A1T; b4.out_mb = s->d1T; b4.zs_act = (long long)s->H1 * B;
         b4.bias_upd = children + s->woff1 + (long long)s->H1 * s->D; b4.zs_bias = s->P;
@@ -482,6 +561,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
             return e;
         // B3: W2 -= η/B · δ2bᵀ·A1
         tc::Epi b3 = base;
+        b3.trace = g_trace ? g_trace + 4 * 16384LL : nullptr;
         b3.M = s->H2; b3.N = s->H1; b3.nvalid = s->H1;
         b3.master = children + s->woff2; b3.zs_master = s->P;
         b3.wb = s->W2b; b3.wbt = odd ? s->W2bT : s->W2bT2; b3.zs_w = (long long)s->H2 * s->H1;
@@ -490,6 +570,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         if ((e = cudaEventRecord(s->ev_b3, s->side))) return e;
         // B5: W1 -= η/B · δ1ᵀ·Xs
         tc::Epi b5 = base;
+        b5.trace = g_trace ? g_trace + 5 * 16384LL : nullptr;
         b5.M = s->H1; b5.N = s->D; b5.nvalid = s->D;
         b5.master = children + s->woff1; b5.zs_master = s->P;
         b5.wb = s->W1b; b5.wbt = nullptr; b5.zs_w = (long long)s->H1 * s->D;

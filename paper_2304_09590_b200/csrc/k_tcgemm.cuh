@@ -27,7 +27,7 @@ constexpr int BK = 64;        // K per stage: 64 bf16 = one 128-byte swizzle row
 // have K = 64, a single stage) so that two CTAs fit per SM
 // threads per CTA: the wide update tiles (BN = 256, memory-bound epilogues) use 8 warps, two
 // per TMEM lane quadrant, each taking half of the columns
-__host__ __device__ constexpr int threads_for(int bn) { return bn >= 256 ? 256 : 128; }
+__host__ __device__ constexpr int threads_for(int bn) { return bn >= 64 ? 256 : 128; }
 __host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? 2 : (bn >= 128 ? 4 : 8); }
 
 enum { EPI_STORE_F32 = 0, EPI_FWD = 1, EPI_BWD = 2, EPI_UPD = 3 };
@@ -67,6 +67,11 @@ struct Epi {
     float lr;
     long long n_local;
     int K_local, step, batch;
+    // debug timeline (nullable; tools/trace_tc.py): per CTA 24 entries — [0] %globaltimer at
+    // entry, then clock64 at: [1] entry, [2] after the prologue, [3] after griddep_wait,
+    // [4 + kt] (kt < 16) each stage's full-barrier wait done (MMA thread), [20] epilogue
+    // start (accumulator complete), [23] first chunk read from TMEM, [22] chunk loop done, [21] end
+    long long* trace;
 };
 
 __device__ __forceinline__ float update_scale(const Epi& ep, int z) {
@@ -173,8 +178,12 @@ struct __align__(1024) GemmSmem {
     uint32_t tmem;
 };
 
+// the wide update tiles run two CTAs per SM (smem 2 × ~97 KB, TMEM 2 × 256 columns): the
+// register budget must allow it (≤ 128 per thread at 2 × 256 threads)
+__host__ __device__ constexpr int min_ctas_for(int bn) { return bn >= 256 ? 2 : 1; }
+
 template <int BN, int EPI>
-__global__ void __launch_bounds__(threads_for(BN))
+__global__ void __launch_bounds__(threads_for(BN), min_ctas_for(BN))
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, Epi ep) {
     extern __shared__ __align__(1024) unsigned char raw[];
     GemmSmem<BN>& s = *reinterpret_cast<GemmSmem<BN>*>(
@@ -183,6 +192,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, z = blockIdx.z + ep.zoff;
     const int nk = (K + BK - 1) / BK;
     constexpr int STAGES = GemmSmem<BN>::STAGES;
+    long long* trc = ep.trace ? ep.trace + 24LL * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z))
+                              : nullptr;
+    auto tstamp = [&](int i) {
+        if (trc) {
+            long long t;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+            trc[i] = t;
+        }
+    };
+    if (trc && threadIdx.x == 0) {
+        long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        trc[0] = g;
+        tstamp(1);
+    }
     constexpr int NWE = threads_for(BN) / 32;     // epilogue warps: 4, or 8 (two per lane quadrant)
     constexpr int CSPAN = BN / (NWE / 4);          // columns per epilogue warp
     static_assert(sizeof(GemmSmem<BN>::a) + sizeof(GemmSmem<BN>::b) >=
@@ -198,21 +222,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc(&s.tmem, BN < 32 ? 32 : BN);
+    if (threadIdx.x == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
     fence_before();
     __syncthreads();
     fence_after();
     const uint32_t tmem = s.tmem;
-    // the next layer's weights of this row tile (EPI_FWD with w3): staged while the MMAs run
-    __shared__ float w3s[EPI == EPI_FWD ? 16 * BM : 1];
-    if constexpr (EPI == EPI_FWD) {
-        if (ep.w3) {
-            for (int i = threadIdx.x; i < 16 * BM; i += blockDim.x) {
-                const int o = i / BM, r = i % BM;
-                w3s[i] = (m0 + r < ep.M) ? __bfloat162float(ep.w3[((long long)z * 16 + o) * ep.M + m0 + r]) : 0.f;
-            }
-        }
-    }
-
+    // everything above overlaps the previous kernel's tail (PDL); every global read and
+    // write below comes after it has completed
+    if (threadIdx.x == 0) tstamp(2);
+    griddep_wait();
+    griddep_launch();
+    if (threadIdx.x == 0) tstamp(3);
+    // the next layer's weights of this row tile (EPI_FWD with w3): staged by warps 2-3 while
+    // the producer and MMA threads run (read after the accumulator barrier)
+    __shared__ __align__(16) float w3s[EPI == EPI_FWD ? 16 * BM : 1];
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
         constexpr uint32_t bytes = (BM + BN) * BK * 2;
@@ -229,6 +255,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         for (int kt = 0; kt < nk; ++kt) {
             const int st = kt % STAGES;
             mbar_wait(&s.full[st], (uint32_t)((kt / STAGES) & 1));
+            if (kt < 16) tstamp(4 + kt);
             fence_after();
             const uint32_t sa = smem_u32(s.a[st]), sb = smem_u32(s.b[st]);
 #pragma unroll
@@ -239,36 +266,104 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         mma_commit(&s.accf);                           // accumulator complete
     }
+    if constexpr (EPI == EPI_FWD) {
+        if (ep.w3 && warp >= 2 && warp < 4) {      // 64 threads × 2 rows × 16 outputs; all loads
+            const int rr = (threadIdx.x - 64) * 2; // issued first (a generic pointer may alias
+                                                   // shared memory: stores would serialise them)
+            uint32_t v[16];
+            const __nv_bfloat16* w3 = ep.w3 + (long long)z * 16 * ep.M + m0 + rr;
+            const bool ok = m0 + rr + 1 < ep.M && ((ep.M & 1) == 0);
+#pragma unroll
+            for (int o = 0; o < 16; ++o)
+                v[o] = ok ? __ldg(reinterpret_cast<const unsigned int*>(w3 + (long long)o * ep.M)) : 0u;
+#pragma unroll
+            for (int o = 0; o < 16; ++o) {
+                float2 f = ok ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[o])) : make_float2(0.f, 0.f);
+                if (!ok) {
+                    if (m0 + rr < ep.M) f.x = __bfloat162float(ep.w3[((long long)z * 16 + o) * ep.M + m0 + rr]);
+                    if (m0 + rr + 1 < ep.M) f.y = __bfloat162float(ep.w3[((long long)z * 16 + o) * ep.M + m0 + rr + 1]);
+                }
+                w3s[rr * 16 + o] = f.x;            // [row][o]: a row's 16 weights are one
+                w3s[(rr + 1) * 16 + o] = f.y;      // broadcast 4 × 16-byte read
+            }
+        }
+    }
     // ---------------- epilogue: all 4 warps ----------------
     // Per 32-column chunk: (1) lane = tile row (the TMEM lane layout): per-row work and the
     // [n][m] outputs, which are coalesced in this mapping; (2) through a padded shared tile,
     // lane = column: the [m][n] outputs, coalesced 128-byte rows.  The operand stages are
     // free once the accumulator is complete, so the transpose tile reuses them.
-    __syncwarp();
-    mbar_wait(&s.accf, 0u);
-    __syncwarp();
-    fence_after();
-    float (*tile)[33] = reinterpret_cast<float (*)[33]>(&s.a[0][0]) + 32 * warp;   // a then b: free now
     const int quad = warp & 3, chalf = warp >> 2;  // TMEM lanes 32·quad.., column half
     const int mrow0 = m0 + 32 * quad;
+    // EPI_UPD: the fp32 master values of the next chunk are loaded one chunk ahead (the first
+    // chunk's while the MMAs run): the epilogue is a chain of memory round trips otherwise.
+    // (Lane = column, 32 rows: each load instruction is one coalesced 128-byte row segment; a
+    // lane-per-row layout with vector accesses touches 32 lines per instruction and ran 1.7x
+    // slower.)
+    float old[EPI == EPI_UPD ? 32 : 1];
+    auto load_old = [&](int c) {
+        if constexpr (EPI == EPI_UPD) {
+            const int n = n0 + c + lane;
+            const float* ms = ep.master + (long long)z * ep.zs_master + (mrow0 * ep.N + n);
+            const bool full = n < ep.nvalid && mrow0 + 32 <= ep.M;
+#pragma unroll
+            for (int r = 0; r < 32; ++r)
+                old[r] = (full || (n < ep.nvalid && mrow0 + r < ep.M)) ? ms[r * ep.N] : 0.f;
+        }
+    };
+    load_old(chalf * CSPAN);
     const int m = mrow0 + lane;                        // phase-1 row of this thread
     const bool mok = m < ep.M;
+    // EPI_FWD / EPI_BWD operands that do not depend on the accumulator, loaded before it is
+    // complete: the bias of this row; the ReLU mask of the first chunk (the next chunk's at
+    // the end of each chunk) and the bias being updated
+    float bias_pre = 0.f;
+    if constexpr (EPI == EPI_FWD) bias_pre = mok ? ep.bias[(long long)z * ep.zs_bias + m] : 0.f;
+    if constexpr (EPI == EPI_BWD) bias_pre = (mok && chalf == 0) ? ep.bias_upd[(long long)z * ep.zs_bias + m] : 0.f;
+    __nv_bfloat16 mv[EPI == EPI_BWD ? 32 : 1];
+    auto load_mask = [&](int c) {
+        if constexpr (EPI == EPI_BWD) {
+            const int n = n0 + c + lane;
+            const __nv_bfloat16* mk = ep.mask + (long long)z * ep.zs_act + (mrow0 * ep.N + n);
+            const int rows = (ep.M - mrow0) < 32 ? (ep.M - mrow0) : 32;
+            const bool full = rows == 32 && n < ep.nvalid;
+#pragma unroll
+            for (int r = 0; r < 32; ++r)
+                mv[r] = (full || (r < rows && n < ep.nvalid)) ? mk[r * ep.N] : __float2bfloat16_rn(0.f);
+        }
+    };
+    load_mask(chalf * CSPAN);
+    __syncwarp();
+    mbar_wait(&s.accf, 0u);
+    if (threadIdx.x == 0) tstamp(20);
+    __syncwarp();
+    fence_after();
+    if constexpr (EPI == EPI_FWD) {
+        if (ep.w3) __syncthreads();                // w3s staged
+    }
+    float (*tile)[33] = reinterpret_cast<float (*)[33]>(&s.a[0][0]) + 32 * warp;   // a then b: free now
     float rowsum = 0.f;
     float scale = 0.f;
     if constexpr (EPI == EPI_UPD || EPI == EPI_BWD) scale = update_scale(ep, z);
+    // the epilogue is latency-bound (few warps): per-CN base pointers once, 32-bit offsets,
+    // and a predicate-free path for full 32-row × 32-column chunks
+    const int Mv = ep.M, Nv = ep.N, NVv = ep.nvalid;
+    const int rows = Mv - mrow0 < 0 ? 0 : (Mv - mrow0 > 32 ? 32 : Mv - mrow0);
 #pragma unroll 1
     for (int c = chalf * CSPAN; c < (chalf + 1) * CSPAN; c += 32) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)c, v);
+        if (threadIdx.x == 0 && c == 0) tstamp(23);
         const int nb = n0 + c;
         // ---- phase 1: lane = row
         if constexpr (EPI == EPI_FWD) {
-            const float b = mok ? ep.bias[(long long)z * ep.zs_bias + m] : 0.f;
-            __nv_bfloat16* obm = ep.out_bm + (long long)z * ep.zs_act;
+            const float b = bias_pre;
+            __nv_bfloat16* obm = ep.out_bm + (long long)z * ep.zs_act + m;   // [n][m]
+            const bool fullc = mok && nb + 32 <= NVv;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const __nv_bfloat16 yb = __float2bfloat16_rn(fmaxf(v[i] + b, 0.f));   // ReLU (Eq.4), bias once (R1)
-                if (mok && nb + i < ep.nvalid) obm[(long long)(nb + i) * ep.M + m] = yb;
+                if (fullc || (mok && nb + i < NVv)) obm[(nb + i) * Mv] = yb;
                 v[i] = __bfloat162float(yb);
             }
         }
@@ -277,18 +372,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         __syncwarp();
         // ---- phase 2: lane = column n = nb + lane
         const int n = nb + lane;
-        const bool nok = n < ep.nvalid;
+        const bool nok = n < NVv;
+        const bool full = nok && rows == 32;
+        const int off0 = mrow0 * Nv + n;               // [m][n] offset of (mrow0, n) in one CN's matrix
         if constexpr (EPI == EPI_STORE_F32) {
-#pragma unroll 4
-            for (int r = 0; r < 32; ++r)
-                if (mrow0 + r < ep.M && nok)
-                    ep.out_f32[(long long)z * ep.zs_out + (long long)(mrow0 + r) * ep.N + n] = tile[r][lane];
+            float* o = ep.out_f32 + (long long)z * ep.zs_out + off0;
+            if (full) {
+#pragma unroll
+                for (int r = 0; r < 32; ++r) o[r * Nv] = tile[r][lane];
+            } else if (nok) {
+#pragma unroll
+                for (int r = 0; r < 32; ++r)
+                    if (r < rows) o[r * Nv] = tile[r][lane];
+            }
         } else if constexpr (EPI == EPI_FWD) {
             if (ep.out_mb) {
-                __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + n;
-#pragma unroll 4
-                for (int r = 0; r < 32; ++r)
-                    if (mrow0 + r < ep.M && nok) omb[(long long)(mrow0 + r) * ep.N] = __float2bfloat16_rn(tile[r][lane]);
+                __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + off0;
+                if (full) {
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) omb[r * Nv] = __float2bfloat16_rn(tile[r][lane]);
+                } else if (nok) {
+#pragma unroll
+                    for (int r = 0; r < 32; ++r)
+                        if (r < rows) omb[r * Nv] = __float2bfloat16_rn(tile[r][lane]);
+                }
             }
             if (ep.w3) {                           // this warp's 32 rows' share of z3[n][o]
                 float zp[16];
@@ -297,9 +404,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll 4
                 for (int r = 0; r < 32; ++r) {
                     const float y = tile[r][lane];
-                    const float* wr = w3s + (32 * quad + r);
+                    const float4* wr = reinterpret_cast<const float4*>(w3s + (32 * quad + r) * 16);
 #pragma unroll
-                    for (int o = 0; o < 16; ++o) zp[o] = fmaf(wr[o * BM], y, zp[o]);
+                    for (int u = 0; u < 4; ++u) {
+                        const float4 w4 = wr[u];
+                        zp[4 * u] = fmaf(w4.x, y, zp[4 * u]);
+                        zp[4 * u + 1] = fmaf(w4.y, y, zp[4 * u + 1]);
+                        zp[4 * u + 2] = fmaf(w4.z, y, zp[4 * u + 2]);
+                        zp[4 * u + 3] = fmaf(w4.w, y, zp[4 * u + 3]);
+                    }
                 }
                 float* zr = reinterpret_cast<float*>(&s.a[0][0]) + NWE * 32 * 33;   // [4][BN][16]
 #pragma unroll
@@ -307,57 +420,53 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         } else if constexpr (EPI == EPI_BWD) {
             // d = acc ⊙ [mask > 0] (ReLU'(z) from the stored activation, R9), mask [m][n]
-            const __nv_bfloat16* mk = ep.mask + (long long)z * ep.zs_act + n;
-            __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + n;
-            const int rows = (ep.M - mrow0) < 32 ? (ep.M - mrow0) : 32;
-            __nv_bfloat16 mv[32];
-#pragma unroll
-            for (int r = 0; r < 32; ++r)
-                mv[r] = (r < rows && nok) ? mk[(long long)(mrow0 + r) * ep.N] : __float2bfloat16_rn(0.f);
+            __nv_bfloat16* omb = ep.out_mb + (long long)z * ep.zs_act + off0;
+            const bool nin = n < Nv;
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
                 const float d = (__bfloat162float(mv[r]) > 0.f) ? tile[r][lane] : 0.f;
                 tile[r][lane] = d;
-                if (r < rows && n < ep.N) omb[(long long)(mrow0 + r) * ep.N] = __float2bfloat16_rn(d);
+                if ((rows == 32 && nin) || (r < rows && nin)) omb[r * Nv] = __float2bfloat16_rn(d);
             }
+            if (c + 32 < (chalf + 1) * CSPAN) load_mask(c + 32);
             __syncwarp();
 #pragma unroll
             for (int i = 0; i < 32; ++i) rowsum += tile[lane][i];     // phase 3: lane = row
         } else {  // EPI_UPD: W -= η·(Σ/B), bf16 copy
-            float* ms = ep.master + (long long)z * ep.zs_master + n;
-            __nv_bfloat16* wb = ep.wb + (long long)z * ep.zs_w + n;
-            const int rows = (ep.M - mrow0) < 32 ? (ep.M - mrow0) : 32;
-            if (nok && rows == 32) {
-                float old[32];
+            float* ms = ep.master + (long long)z * ep.zs_master + off0;
+            __nv_bfloat16* wb = ep.wb + (long long)z * ep.zs_w + off0;
+            auto upd = [&](int r) {
+                const float w = fmaf(-scale, tile[r][lane], old[r]);
+                ms[r * Nv] = w;
+                const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
+                wb[r * Nv] = w16;
+                tile[r][lane] = __bfloat162float(w16);
+            };
+            if (full) {
 #pragma unroll
-                for (int r = 0; r < 32; ++r) old[r] = ms[(long long)(mrow0 + r) * ep.N];
-#pragma unroll
-                for (int r = 0; r < 32; ++r) {
-                    const float w = fmaf(-scale, tile[r][lane], old[r]);
-                    ms[(long long)(mrow0 + r) * ep.N] = w;
-                    const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
-                    wb[(long long)(mrow0 + r) * ep.N] = w16;
-                    tile[r][lane] = __bfloat162float(w16);
-                }
+                for (int r = 0; r < 32; ++r) upd(r);
             } else if (nok) {
-                for (int r = 0; r < rows; ++r) {
-                    const float w = fmaf(-scale, tile[r][lane], ms[(long long)(mrow0 + r) * ep.N]);
-                    ms[(long long)(mrow0 + r) * ep.N] = w;
-                    const __nv_bfloat16 w16 = __float2bfloat16_rn(w);
-                    wb[(long long)(mrow0 + r) * ep.N] = w16;
-                    tile[r][lane] = __bfloat162float(w16);
-                }
+#pragma unroll
+                for (int r = 0; r < 32; ++r)
+                    if (r < rows) upd(r);
             }
+            if (c + 32 < (chalf + 1) * CSPAN) load_old(c + 32);
             if (ep.wbt) {                              // ---- phase 3: lane = row again, [n][m] copy
                 __syncwarp();
                 __nv_bfloat16* wt = ep.wbt + (long long)z * ep.zs_w + m;
-#pragma unroll 4
-                for (int i = 0; i < 32; ++i)
-                    if (mok && nb + i < ep.nvalid) wt[(long long)(nb + i) * ep.M] = __float2bfloat16_rn(tile[lane][i]);
+                if (mok && nb + 32 <= NVv) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) wt[(nb + i) * Mv] = __float2bfloat16_rn(tile[lane][i]);
+                } else if (mok) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (nb + i < NVv) wt[(nb + i) * Mv] = __float2bfloat16_rn(tile[lane][i]);
+                }
             }
         }
         __syncwarp();
     }
+    if (threadIdx.x == 0) tstamp(22);
     if constexpr (EPI == EPI_FWD) {
         if (ep.w3) {                               // sum the 4 row groups, in order
             __syncthreads();
@@ -370,11 +479,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
     }
     if constexpr (EPI == EPI_BWD) {
-        if (mok && chalf == 0) ep.bias_upd[(long long)z * ep.zs_bias + m] -= scale * rowsum;   // b -= η·(Σδ/B)
+        if constexpr (NWE == 8) {                  // the two column halves of a row, in order
+            float* rs = reinterpret_cast<float*>(&s.b[0][0]);
+            if (chalf == 1) rs[32 * quad + lane] = rowsum;
+            __syncthreads();
+            if (chalf == 0) rowsum += rs[32 * quad + lane];
+        }
+        if (mok && chalf == 0) ep.bias_upd[(long long)z * ep.zs_bias + m] = bias_pre - scale * rowsum;   // b -= η·(Σδ/B)
     }
     fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+    if (threadIdx.x == 0) tstamp(21);
 }
 
 template <int BN>

@@ -552,7 +552,7 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
     // copy_stream while group g-1 trains on the caller's stream.  A group must still fill
     // the GPU: the batched mini-batch paths take every CN at once (one group), the cluster
     // kernels run ~148/cluster CNs concurrently.
-    int groups = 1;
+    int groups = 1, gsize = net->K_local;
     {
         ResidentPlan rp{};
         int var = PNN_VARIANT_AUTO;
@@ -564,8 +564,13 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
                                                          : plan_cluster(net->d, net->batch).cluster);
         else if (k == PNN_KERNEL_REFERENCE) cap = 148;
         else if (k == PNN_KERNEL_MB_RESIDENT) cap = 148 / mbres_cluster(net->d);
-        groups = net->K_local / (cap > 0 ? cap : 1);
-        groups = groups < 1 ? 1 : (groups > 8 ? 8 : groups);
+        // groups of whole waves: a multiple of `cap` CNs each (a group that is a wave and a bit
+        // runs two waves), at most 8 groups
+        cap = cap > 0 ? cap : 1;
+        const int waves = (net->K_local + cap - 1) / cap;
+        gsize = cap * ((waves + 7) / 8);
+        if (gsize > net->K_local) gsize = net->K_local;
+        groups = (net->K_local + gsize - 1) / gsize;
     }
     const size_t row_bytes = sizeof(float) * net->d.n[0];
     // Events and the copy stream are released on every return path: the copies already
@@ -591,8 +596,8 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
     // the previous call's launches (on any stream) may still read the staging buffers
     CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, net->stage_released, 0));
     for (int g = 0; g < groups; ++g) {
-        const int s0 = (int)((long long)g * net->K_local / groups);
-        const int s1 = (int)((long long)(g + 1) * net->K_local / groups);
+        const int s0 = g * gsize;
+        const int s1 = (g + 1) * gsize < net->K_local ? (g + 1) * gsize : net->K_local;
         long long r0, c0, r1, c1;
         shard_of(n, net->K_local, s0, &r0, &c0);
         shard_of(n, net->K_local, s1 - 1, &r1, &c1);
