@@ -542,6 +542,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         f2.bias = children + s->woff2 + (long long)s->H2 * s->H1; f2.zs_bias = s->P;
         f2.out_bm = s->A2; f2.out_mb = nullptr; f2.zs_act = (long long)s->H2 * B;
         f2.w3 = s->W3b; f2.z3part = s->z3part;          // the output layer's partials, fused
+        f2.a_early = true;                                // W2b: B3 of step j-1, joined before F1(j)
         if ((e = launch_gemm<64, tc::EPI_FWD>(s->tW2b, s->tA1, s_count, s->H2, B, s->H1, f2, st))) return e;
         // output layer (CUDA cores: N = 10 / K = 10 are not dense contractions)
         if ((e = launch_pdl(mb_out_bwd, dim3((unsigned)(s->H2 / 64), (unsigned)s_count), dim3(512), 0, st,
@@ -554,6 +555,7 @@ static cudaError_t enqueue_epoch(MbState* s, float* children, const float* x, co
         tc::Epi b4 = base;
         b4.trace = g_trace ? g_trace + 3 * 16384LL : nullptr;
         b4.M = s->H1; b4.N = B; b4.nvalid = B;
+        b4.a_early = true;                                // W2bT copy: B3 of step j-1
         b4.mask = s->A1T; b4.out_mb = s->d1T; b4.zs_act = (long long)s->H1 * B;
         b4.bias_upd = children + s->woff1 + (long long)s->H1 * s->D; b4.zs_bias = s->P;
         if ((e = launch_gemm<64, tc::EPI_BWD>(odd ? s->tW2bT2 : s->tW2bT, s->td2b, s_count, s->H1, B, s->H2, b4,

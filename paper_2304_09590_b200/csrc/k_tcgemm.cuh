@@ -67,6 +67,10 @@ struct Epi {
     float lr;
     long long n_local;
     int K_local, step, batch;
+    // A (the weight operand) was complete before the previous kernel of the stream started
+    // (it comes from an earlier kernel or another stream's joined kernel): its first stages'
+    // loads may be issued before griddep_wait, under the previous kernel's tail (PDL)
+    bool a_early;
     // debug timeline (nullable; tools/trace_tc.py): per CTA 24 entries — [0] %globaltimer at
     // entry, then clock64 at: [1] entry, [2] after the prologue, [3] after griddep_wait,
     // [4 + kt] (kt < 16) each stage's full-barrier wait done (MMA thread), [20] epilogue
@@ -233,6 +237,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // everything above overlaps the previous kernel's tail (PDL); every global read and
     // write below comes after it has completed
     if (threadIdx.x == 0) tstamp(2);
+    constexpr uint32_t kStageBytes = (BM + BN) * BK * 2;
+    const int npre = ep.a_early ? (nk < STAGES ? nk : STAGES) : 0;
+    if (warp == 0 && lane == 0) {
+        for (int kt = 0; kt < npre; ++kt) {        // stage kt: expect A and B, issue A now
+            mbar_arrive_expect_tx(&s.full[kt], kStageBytes);
+            tma_load_3d(s.a[kt], &tmA, kt * BK, m0, z, &s.full[kt]);
+        }
+    }
     griddep_wait();
     griddep_launch();
     if (threadIdx.x == 0) tstamp(3);
@@ -241,12 +253,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     __shared__ __align__(16) float w3s[EPI == EPI_FWD ? 16 * BM : 1];
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer ----------------
-        constexpr uint32_t bytes = (BM + BN) * BK * 2;
         for (int kt = 0; kt < nk; ++kt) {
             const int st = kt % STAGES;
             if (kt >= STAGES) mbar_wait(&s.empty[st], (uint32_t)(((kt / STAGES) - 1) & 1));
-            mbar_arrive_expect_tx(&s.full[st], bytes);
-            tma_load_3d(s.a[st], &tmA, kt * BK, m0, z, &s.full[st]);
+            if (kt >= npre) {
+                mbar_arrive_expect_tx(&s.full[st], kStageBytes);
+                tma_load_3d(s.a[st], &tmA, kt * BK, m0, z, &s.full[st]);
+            }
             tma_load_3d(s.b[st], &tmB, kt * BK, n0, z, &s.full[st]);
         }
     } else if (warp == 1 && lane == 0) {
