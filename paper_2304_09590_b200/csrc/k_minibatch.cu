@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(512) mb_out_bwd(float* __restrict__ children, 
                                                   MbState s, long long n_local, int K_local, int z0, int step,
                                                   float lr, long long* trace) {
     // debug timeline (nullable; tools/trace_tc.py): per CTA [0] %globaltimer at entry, clock64 at
-    // [1] entry, [2] after griddep_wait, [3] δ3 ready, [4] end
+    // [1] entry, [2] after griddep_wait, [5] operands loaded, [6] z3 summed, [7] δ3 formed,
+    // [3] δ3 shared, [4] end
     long long* trc = (trace && threadIdx.x == 0) ? trace + 24LL * (blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
     auto tstamp = [&](int i) {
         if (trc) {
@@ -409,7 +410,6 @@ __global__ void __launch_bounds__(512) mb_out_bwd(float* __restrict__ children, 
 #pragma unroll
         for (int o = 0; o < 16; ++o)
             if (o < s.O) { zz[o] = bb[o] + zz[o]; m = fmaxf(m, zz[o]); }
-        if (m == 12345.f) tstamp(9);               // (never: keeps the next stamp after the sums)
         tstamp(6);
         float sum = 0.f;
 #pragma unroll
