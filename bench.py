@@ -190,7 +190,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "reference", "resident", "cluster"])
     ap.add_argument("--variant", default="auto",
-                    choices=["auto", "v8", "v10", "tmem", "cluster", "deep", "mb_step", "mb_resident"])
+                    choices=["auto", "v8", "v10", "tmem", "ws", "cluster", "deep", "mb_step", "mb_resident"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -379,6 +379,10 @@ def main():
                                2: ("persistent SGD launch, TMEM variant (k_tmem.cu: one SM per CN, W1 in "
                                    "registers + tensor memory, Gram terms formed in the launch)"
                                    if variant_id == 11 else
+                                   "persistent SGD launch, warp-specialised TMEM variant (k_ws.cu: one SM per CN, "
+                                   "W1 in registers + tensor memory + shared memory, the per-sample chain on its own "
+                                   "warpgroup, Gram terms formed in the launch)"
+                                   if variant_id == 12 else
                                    "persistent SGD launch (library CUDA events around it; frac_epoch adds the "
                                    "Gram pre-pass)"),
                                5: ("training epoch (deep cluster variant: Gram pre-pass + W1 in the registers and "
@@ -417,7 +421,7 @@ def main():
                                    f"lr {cfg.lr}",
                        "K_local": K_local, "rows_per_rank": nrows, "test_rows": cfg.n_test,
                        "kernel": ["auto", "reference", "resident", "tc_bf16", "mb_f32", "cluster", "mb_resident"][kernel_id],
-                       "variant": {0: "none", 8: "v8", 10: "v10", 11: "tmem", 20: "cluster", 21: "deep",
+                       "variant": {0: "none", 8: "v8", 10: "v10", 11: "tmem", 12: "ws", 20: "cluster", 21: "deep",
                                    30: "mb_step", 31: "mb_resident"}.get(variant_id, str(variant_id)),
                        "l2": f"inputs {X.nbytes / 2**20:.0f} MiB per rank > 126 MB L2 (no flush)"},
             "roofline": roof,

@@ -125,6 +125,9 @@ enum { PNN_VARIANT_AUTO = 0,             /* the family's AUTO rule              
        PNN_VARIANT_RESIDENT_V10 = 10,    /* sweep CTA(s) + a dedicated chain CTA */
        PNN_VARIANT_RESIDENT_TMEM = 11,   /* one SM per CN: W1 in registers and
                                             tensor memory (H <= 128)            */
+       PNN_VARIANT_RESIDENT_WS = 12,     /* as TMEM, warp-specialised: sweeps and
+                                            the per-sample chain on separate
+                                            warpgroups (H <= 128)               */
        PNN_VARIANT_CLUSTER_GENERIC = 20, /* any depth, weights in shared memory  */
        PNN_VARIANT_CLUSTER_DEEP = 21,    /* 3-layer nets, W1 in registers       */
        PNN_VARIANT_MB_STEP = 30,         /* fp32 mini-batch: step kernels       */

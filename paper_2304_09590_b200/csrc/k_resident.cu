@@ -1122,7 +1122,7 @@ ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int vari
         return p;
     };
     if (variant != PNN_VARIANT_AUTO && variant != PNN_VARIANT_RESIDENT_V8 && variant != PNN_VARIANT_RESIDENT_V10 &&
-        variant != PNN_VARIANT_RESIDENT_TMEM)
+        variant != PNN_VARIANT_RESIDENT_TMEM && variant != PNN_VARIANT_RESIDENT_WS)
         return no("not a resident-kernel variant");
     if (batch != 1) return no("mini-batch runs on the reference kernel");
     if (d.L != 2) return no("resident kernel covers 2-layer nets (D-H-O)");
@@ -1157,6 +1157,7 @@ ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int vari
         else v = PNN_VARIANT_RESIDENT_V8;
     }
     if (v == PNN_VARIANT_RESIDENT_TMEM && !tm_ok) return no("TMEM variant: hidden layer wider than 128");
+    if (v == PNN_VARIANT_RESIDENT_WS && ws_plan(d, batch) != nullptr) return no("WS variant: hidden layer wider than 128");
     if (v == PNN_VARIANT_RESIDENT_V10 && !v10_ok) return no("v10 variant: hidden layer wider than 128");
     p.groups = 1;
     p.threads = NW * 32;                           // 8 warps; rows >= U are idle
@@ -1168,6 +1169,11 @@ ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int vari
         p.variant = 10;
         p.cluster = c10;
         p.smem = kSplitHead + sizeof(float) * (size_t)(S + 1) * DP;   // + the zero row (paired sweeps)
+    } else if (v == PNN_VARIANT_RESIDENT_WS) {
+        p.variant = 12;
+        p.cluster = 1;
+        p.threads = 384;
+        p.smem = 0;                                // sized by launch_sgd_ws
     } else {
         p.variant = 11;
         p.cluster = 1;
@@ -1187,9 +1193,10 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 cudaEvent_t ev0, cudaEvent_t ev1) {
     if (s_count <= 0) return cudaSuccess;
     cudaError_t e;
-    if (p.variant == 11) {                         // v11 forms its Gram terms in the launch
+    if (p.variant == 11 || p.variant == 12) {      // v11 / v12 form their Gram terms in the launch
         if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
-        e = launch_sgd_tmem(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st);
+        e = p.variant == 11 ? launch_sgd_tmem(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st)
+                            : launch_sgd_ws(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st);
         if (e != cudaSuccess || !ev1) return e;
         return cudaEventRecord(ev1, st);
     }

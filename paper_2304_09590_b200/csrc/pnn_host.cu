@@ -165,7 +165,8 @@ pnn_status alloc_local(pnn_net net) {
 }
 
 bool is_resident_variant(int v) {
-    return v == PNN_VARIANT_RESIDENT_V8 || v == PNN_VARIANT_RESIDENT_V10 || v == PNN_VARIANT_RESIDENT_TMEM;
+    return v == PNN_VARIANT_RESIDENT_V8 || v == PNN_VARIANT_RESIDENT_V10 || v == PNN_VARIANT_RESIDENT_TMEM ||
+           v == PNN_VARIANT_RESIDENT_WS;
 }
 
 // The kernel family (PNN_KERNEL_*, -1 when a forced choice does not fit) and, in *var, the
@@ -204,7 +205,8 @@ int choose_kernel(pnn_net net, ResidentPlan* plan, int* var = nullptr) {
     *plan = plan_resident(net->d, net->batch, conc, is_resident_variant(fv) ? fv : PNN_VARIANT_AUTO);
     if (plan->ok)
         v = plan->variant == 8 ? PNN_VARIANT_RESIDENT_V8
-            : plan->variant == 10 ? PNN_VARIANT_RESIDENT_V10 : PNN_VARIANT_RESIDENT_TMEM;
+            : plan->variant == 10 ? PNN_VARIANT_RESIDENT_V10
+            : plan->variant == 12 ? PNN_VARIANT_RESIDENT_WS : PNN_VARIANT_RESIDENT_TMEM;
     if (net->kernel == PNN_KERNEL_RESIDENT) return plan->ok ? PNN_KERNEL_RESIDENT : -1;
     if (plan->ok) return PNN_KERNEL_RESIDENT;
     v = PNN_VARIANT_AUTO;
@@ -243,7 +245,8 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         if (k != PNN_KERNEL_RESIDENT) CUDA_TRY(net, cudaEventRecord(ev0, st));   // the resident path
     }                                                                               // brackets its SGD launch
     const bool deep = var == PNN_VARIANT_CLUSTER_DEEP;
-    const bool gram = deep || (k == PNN_KERNEL_RESIDENT && var != PNN_VARIANT_RESIDENT_TMEM);
+    const bool gram = deep || (k == PNN_KERNEL_RESIDENT && var != PNN_VARIANT_RESIDENT_TMEM &&
+                               var != PNN_VARIANT_RESIDENT_WS);
     if (gram && net->gram_rows < n) {                                // 32-B Gram records (R27)
         cudaFree(net->d_gram);
         net->d_gram = nullptr;
@@ -448,7 +451,8 @@ pnn_status pnn_set_variant(pnn_net net, int32_t variant) {
         break;
     case PNN_VARIANT_RESIDENT_V8:
     case PNN_VARIANT_RESIDENT_V10:
-    case PNN_VARIANT_RESIDENT_TMEM: {
+    case PNN_VARIANT_RESIDENT_TMEM:
+    case PNN_VARIANT_RESIDENT_WS: {
         ResidentPlan p = plan_resident(net->d, net->batch, 0, variant);
         if (!p.ok) return fail(net, PNN_ERR_INVALID, "variant %d not valid: %s", variant, p.why);
         net->kernel = PNN_KERNEL_RESIDENT;
@@ -775,7 +779,8 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     // resident v8 / v10 and the deep cluster variant: Gram terms + training; the TMEM variant
     // forms its Gram terms in the training launch; tc bf16: 7 per mini-batch step; fp32 step
     // kernels: 4 per step; MB_RESIDENT: 1 per epoch
-    const bool gram = v == PNN_VARIANT_CLUSTER_DEEP || (k == PNN_KERNEL_RESIDENT && v != PNN_VARIANT_RESIDENT_TMEM);
+    const bool gram = v == PNN_VARIANT_CLUSTER_DEEP ||
+                      (k == PNN_KERNEL_RESIDENT && v != PNN_VARIANT_RESIDENT_TMEM && v != PNN_VARIANT_RESIDENT_WS);
     *launches = gram ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
     return PNN_OK;
 }

@@ -66,6 +66,12 @@ const char* tmem_plan(const NetDesc& d, int batch);
 cudaError_t launch_sgd_tmem(const NetDesc& d, float* children, const float* x, const int32_t* y, long long n_local,
                             int K_local, int s_first, int s_count, float lr, cudaStream_t st);
 
+// Warp-specialised TMEM variant (k_ws.cu, v12): as v11 with the per-sample chain on its own
+// warpgroup.  nullptr when the shape is supported.
+const char* ws_plan(const NetDesc& d, int batch);
+cudaError_t launch_sgd_ws(const NetDesc& d, float* children, const float* x, const int32_t* y, long long n_local,
+                          int K_local, int s_first, int s_count, float lr, cudaStream_t st);
+
 // The lookahead's Gram records (32 B per row: x(u-4..u-1)·x(u) and the label), k_resident.cu.
 cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
                         int s_count, float4* rec, cudaStream_t st);

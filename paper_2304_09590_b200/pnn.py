@@ -25,9 +25,10 @@ PNN_FP32, PNN_BF16 = 0, 1
 PNN_KERNEL_AUTO, PNN_KERNEL_REFERENCE, PNN_KERNEL_RESIDENT, PNN_KERNEL_TC_BF16, PNN_KERNEL_MB_F32, \
     PNN_KERNEL_CLUSTER, PNN_KERNEL_MB_RESIDENT = 0, 1, 2, 3, 4, 5, 6
 PNN_VARIANT_AUTO, PNN_VARIANT_RESIDENT_V8, PNN_VARIANT_RESIDENT_V10, PNN_VARIANT_RESIDENT_TMEM = 0, 8, 10, 11
+PNN_VARIANT_RESIDENT_WS = 12
 PNN_VARIANT_CLUSTER_GENERIC, PNN_VARIANT_CLUSTER_DEEP, PNN_VARIANT_MB_STEP, PNN_VARIANT_MB_RESIDENT = 20, 21, 30, 31
 VARIANT = {"auto": PNN_VARIANT_AUTO, "v8": PNN_VARIANT_RESIDENT_V8, "v10": PNN_VARIANT_RESIDENT_V10,
-           "tmem": PNN_VARIANT_RESIDENT_TMEM, "cluster": PNN_VARIANT_CLUSTER_GENERIC, "deep": PNN_VARIANT_CLUSTER_DEEP,
+             "tmem": PNN_VARIANT_RESIDENT_TMEM, "ws": PNN_VARIANT_RESIDENT_WS, "cluster": PNN_VARIANT_CLUSTER_GENERIC, "deep": PNN_VARIANT_CLUSTER_DEEP,
            "mb_step": PNN_VARIANT_MB_STEP, "mb_resident": PNN_VARIANT_MB_RESIDENT}
 ACT = {"sigmoid": PNN_SIGMOID, "tanh": PNN_TANH, "relu": PNN_RELU, "softmax": PNN_SOFTMAX,
        "leaky_relu": PNN_LEAKY_RELU}

@@ -186,14 +186,14 @@ def test_cluster_kernel(orc, name, K, n, epochs):
     assert np.abs(merged - omerged).max() < TOL
 
 
-@pytest.mark.parametrize("kernel", ["resident", "v8", "tmem", "cluster", "reference"])
+@pytest.mark.parametrize("kernel", ["resident", "v8", "tmem", "ws", "cluster", "reference"])
 @pytest.mark.parametrize("rows_per_cn", [1, 2, 3, 4, 5, 6, 17])
 def test_short_slices(orc, kernel, rows_per_cn):
     """Slices shorter than the resident kernels' lookahead / prefetch depths (L = 4,
     8 rows in flight) and the cluster kernel's ring, with one ragged slice.  6 CNs fit
-    the GPU, so AUTO's resident plan is v10; v8 / tmem force those variants."""
+    the GPU, so AUTO's resident plan is v10; v8 / tmem / ws force those variants."""
     variant = None
-    if kernel in ("v8", "tmem"):
+    if kernel in ("v8", "tmem", "ws"):
         variant, kernel = kernel, "resident"
     c = CONFIGS["C4"]
     K = 6
@@ -238,6 +238,21 @@ def test_resident_tmem_variant(orc, name, act, K, n):
     X, y = make_split(n, "train", 0)
     net, kids, merged = _train(c.layers, act, c.init, K, c.lr, X, y, 1, "resident", variant="tmem")
     assert net.kernel_variant() == 11 and net.kernel_info() == (2, 1)
+    okids, omerged = orc.train_pnn(c.layers, act, c.init, K, c.lr, 0, X, y, threads=8)
+    err = np.abs(kids - okids).max(axis=1)
+    assert err.max() < TOL, f"per-CN max-abs {err}"
+    assert np.abs(merged - omerged).max() < TOL
+
+
+@pytest.mark.parametrize("name,act,K,n", TMEM_CASES)
+def test_resident_ws_variant(orc, name, act, K, n):
+    """The warp-specialised TMEM variant (v12, k_ws.cu: v11's W1 placement plus one row per
+    warp in shared memory, the per-sample chain on its own warpgroup) vs the oracle."""
+    c = CONFIGS[name]
+    act = act or c.act
+    X, y = make_split(n, "train", 0)
+    net, kids, merged = _train(c.layers, act, c.init, K, c.lr, X, y, 1, "resident", variant="ws")
+    assert net.kernel_variant() == 12 and net.kernel_info() == (2, 1)
     okids, omerged = orc.train_pnn(c.layers, act, c.init, K, c.lr, 0, X, y, threads=8)
     err = np.abs(kids - okids).max(axis=1)
     assert err.max() < TOL, f"per-CN max-abs {err}"
