@@ -1193,10 +1193,10 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 cudaEvent_t ev0, cudaEvent_t ev1) {
     if (s_count <= 0) return cudaSuccess;
     cudaError_t e;
-    if (p.variant == 11 || p.variant == 12) {      // v11 / v12 form their Gram terms in the launch
+    if (p.variant == 11 || (p.variant == 12 && !kWsPrepass)) {   // v11 forms its Gram terms in the launch
         if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
         e = p.variant == 11 ? launch_sgd_tmem(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st)
-                            : launch_sgd_ws(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st);
+                            : launch_sgd_ws(d, children, x, labels, nullptr, n_local, K_local, s_first, s_count, lr, st);
         if (e != cudaSuccess || !ev1) return e;
         return cudaEventRecord(ev1, st);
     }
@@ -1215,6 +1215,7 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
 static cudaError_t launch_sgd_resident_only(const ResidentPlan& p, const NetDesc& d, float* children,
                                             const float* x, const float4* rec, long long n_local, int K_local,
                                             int s_first, int s_count, float lr, cudaStream_t st) {
+    if (p.variant == 12) return launch_sgd_ws(d, children, x, nullptr, rec, n_local, K_local, s_first, s_count, lr, st);
     if (p.variant == 10) {
         if (p.cluster == 2) return launch_split<1>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);
         if (p.cluster == 3) return launch_split<2>(p, d, children, x, rec, n_local, K_local, s_first, s_count, lr, st);

@@ -33,6 +33,9 @@
 #include "pnn_ptx.cuh"
 #include "pnn_tmem.cuh"
 
+#ifndef PNN_WS_EXP
+#define PNN_WS_EXP 0   // experiment builds only: 1 = sweeps without FMAs, 2 = chain without compute
+#endif
 namespace {
 
 using namespace ptx;
@@ -40,28 +43,37 @@ using namespace ptx;
 constexpr int NSW = 8;          // sweep warps (warpgroups 0, 1)
 constexpr int NCW = 4;          // chain warps (warpgroup 2)
 constexpr int NT = 32 * (NSW + NCW);
-constexpr int RR = 5;           // W¹ rows per sweep warp in registers
+#ifndef PNN_WS_SMEM_ROWS
+#define PNN_WS_SMEM_ROWS 3
+#endif
+constexpr int NSR = PNN_WS_SMEM_ROWS;   // W¹ rows per sweep warp in shared memory (its last rows)
 constexpr int TR = 10;          // W¹ rows per sweep warp in TMEM
-constexpr int SR = RR + TR;     // the warp's row in shared memory (its last row)
-constexpr int RPW = RR + TR + 1;// rows per sweep warp
+constexpr int RR = 6 - NSR;     // W¹ rows per sweep warp in registers
+constexpr int SR = RR + TR;     // the warp's first row in shared memory
+constexpr int RPW = RR + TR + NSR;  // rows per sweep warp (16)
 constexpr int UMAX = NSW * RPW; // 128 hidden units
 constexpr int NQ = 6;           // column quads per lane: columns [0, 768)
 constexpr int NP = 2 * NQ;      // f32x2 pairs per lane per row
 constexpr int XC = 768;         // first tail column
 constexpr int DP = 800;         // x ring slot stride (floats)
+constexpr int GOFF = 784;       // PRE: the Gram record of x(u) at its slot + GOFF
 constexpr int LAG = 4;          // lookahead L
 constexpr int S = 16;           // x ring slots (+ one zero row at slot S)
 constexpr int PF = 8;           // prefetch distance: x(c+PF) issued after chain c
 constexpr int O = 10;           // outputs
 constexpr int AR = 8;           // row-sum ring slots (> L)
 constexpr int GR = 8;           // g ring slots (> L)
-constexpr int GT = 4;           // Gram-term ring slots
+constexpr int GT = 8;           // Gram-term ring slots (> L)
 constexpr int TQCOLS = 4 * TR;  // TMEM columns per quad
 constexpr int TTAIL = NQ * TQCOLS;
 // Register budgets per thread.  The launch gives every thread 168 (384 threads, one CTA per
 // SM); setmaxnreg moves them between warpgroups: 2·kSweepRegs + kChainRegs <= 3·168.
-constexpr int kSweepRegs = 224;
-constexpr int kChainRegs = 56;
+#ifndef PNN_WS_SWEEP_REGS
+#define PNN_WS_SWEEP_REGS 224
+#define PNN_WS_CHAIN_REGS 56
+#endif
+constexpr int kSweepRegs = PNN_WS_SWEEP_REGS;
+constexpr int kChainRegs = PNN_WS_CHAIN_REGS;
 static_assert(2 * kSweepRegs + kChainRegs <= 3 * 168, "register pool");
 static_assert(TTAIL + 8 <= 256, "TMEM half of a lane quadrant");
 static_assert(S >= PF + LAG + 4, "x ring: a refilled slot is no longer read");
@@ -75,9 +87,9 @@ struct __align__(16) Smem {
     float asum[AR][UMAX];       // [s % AR][unit] row sums W¹(s-L)·x(s)
     float gbuf[GR][UMAX];       // [c % GR][unit] g(c) = η δ1(c)
     float zp[2][NCW][16];       // [c & 1][chain warp][o] partial logits
-    float gterm[GT][4];         // [s % GT][k-1] G(s-k, s)
+    float gpart[GT][8];         // [s % GT][j] j < 4: G(s-1-j, s); 4 + w: chain warp w's quarter of G(s-5, s)
     float b2s[2][12];           // b2 before sample c at [c & 1]
-    float4 wsm[NSW][NQ][32];    // [warp][quad][lane] columns 4·lane + 128·quad .. +3 of row SR
+    float4 wsm[NSW][NSR][NQ][32];   // [warp][row - SR][quad][lane] columns 4·lane + 128·quad .. +3
 };
 constexpr size_t kSmemHead = ((sizeof(Smem) + 127) / 128) * 128;
 
@@ -127,10 +139,12 @@ __device__ __forceinline__ float treduce16(const float (&v)[16], int lane) {
     return (b1 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? u2[0] : u2[1], 2);
 }
 
-template <int A1, int A2>
+// PRE: the Gram terms and the label come with x(u) through the ring as the 32-B record of
+// gram_kernel (k_resident.cu; launch_gram) instead of being formed by the chain warps.
+template <int A1, int A2, bool PRE>
 __global__ void __launch_bounds__(NT, 1)
 sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ X, const int32_t* __restrict__ Y,
-              long long n_local, int K_local, int s_first, float lr) {
+              const float4* __restrict__ rec, long long n_local, int K_local, int s_first, float lr) {
     extern __shared__ __align__(128) unsigned char smraw[];
     Smem& sm = *reinterpret_cast<Smem*>(smraw);
     float* xring = reinterpret_cast<float*>(smraw + kSmemHead);
@@ -158,7 +172,6 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < (S + 1) * DP; i += blockDim.x) xring[i] = 0.f;   // + the zero row
-    for (int i = threadIdx.x; i < GT * 4; i += blockDim.x) (&sm.gterm[0][0])[i] = 0.f;   // G(·, 0) = 0
     for (int i = threadIdx.x; i < 24; i += blockDim.x) (&sm.b2s[0][0])[i] = (i < O) ? b2g[i] : 0.f;
     fence_proxy_async_smem();
     tmem::fence_before();
@@ -194,14 +207,15 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
             tmem::st32(tq + q * TQCOLS, tv);
             tmem::st8(tq + q * TQCOLS + 32, tv + 32);
         }
-        {
-            const bool live = kr0 + SR < H;
-            const float* src = W1 + (long long)(kr0 + SR) * D + 4 * lane;
+#pragma unroll
+        for (int j = 0; j < NSR; ++j) {
+            const bool live = kr0 + SR + j < H;
+            const float* src = W1 + (long long)(kr0 + SR + j) * D + 4 * lane;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const float2 a = live ? *reinterpret_cast<const float2*>(src + 128 * q) : make_float2(0.f, 0.f);
                 const float2 b = live ? *reinterpret_cast<const float2*>(src + 128 * q + 2) : make_float2(0.f, 0.f);
-                sm.wsm[warp][q][lane] = make_float4(a.x, a.y, b.x, b.y);
+                sm.wsm[warp][j][q][lane] = make_float4(a.x, a.y, b.x, b.y);
             }
         }
         const int trow = lane >> 1, th8 = lane & 1;     // tail: row kr0 + trow, columns 768 + 8·th8 .. +7
@@ -215,106 +229,174 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
         }
         tmem::wait_st();
 
-        for (int s = 0; s < T + LAG; ++s) {
-            if (s < T) {
-                // ---------------- F(s): acc = W¹(s-L)·x(s) ----------------
-                const int sl = s % S;
-                mbar_wait(&sm.xfull[sl], (uint32_t)((s / S) & 1));
-                const float* xn = xring + sl * DP + 4 * lane;
-                uint64_t acc[RPW];
+        // Paired sweeps: step p runs F for samples 2p, 2p+1 in one pass over W¹ (both x rows per
+        // quad, 4 fma.rn.f32x2 per row per quad), then U for samples 2p-4, 2p-3 (in sample order).
+        // F(2p), F(2p+1) see W¹(2p-4): sample 2p misses 4 updates, 2p+1 misses 5 (R27; the chain
+        // applies 4 / 5 Gram corrections).
+        const int npair = (T + 1) >> 1;
+        const int trs = lane & 1;                       // F's reduce: lane l ends with (row l >> 1, sample l & 1)
+        for (int p = 0; p < npair + 2; ++p) {
+            if (p < npair) {
+                // ---------------- F(2p), F(2p+1): acc = W¹(2p-4)·x ----------------
+                const int s0 = 2 * p, s1 = s0 + 1;
+                const bool v1 = s1 < T;
+                const int sl0 = s0 % S, sl1 = v1 ? s1 % S : S;   // slot S: the zero row
+                mbar_wait(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
+                if (v1) mbar_wait(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
+                const float* xn0 = xring + sl0 * DP + 4 * lane;
+                const float* xn1 = xring + sl1 * DP + 4 * lane;
+                uint64_t acc0[RPW], acc1[RPW];
 #pragma unroll
-                for (int r = 0; r < RPW; ++r) acc[r] = 0ull;
+                for (int r = 0; r < RPW; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
+                for (int q = 0; q < (PNN_WS_EXP == 1 ? 0 : NQ); ++q) {
                     uint32_t tv[TQCOLS];
                     tmem::ld32(tq + q * TQCOLS, tv);
                     tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
-                    uint64_t xa, xb;
-                    lds4(xn + 128 * q, xa, xb);
+                    uint64_t xa, xb, ya, yb;
+                    lds4(xn0 + 128 * q, xa, xb);
+                    lds4(xn1 + 128 * q, ya, yb);
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
-                        acc[r] = ffma2(w[r][2 * q], xa, acc[r]);
-                        acc[r] = ffma2(w[r][2 * q + 1], xb, acc[r]);
+                        acc0[r] = ffma2(w[r][2 * q], xa, acc0[r]);
+                        acc1[r] = ffma2(w[r][2 * q], ya, acc1[r]);
+                        acc0[r] = ffma2(w[r][2 * q + 1], xb, acc0[r]);
+                        acc1[r] = ffma2(w[r][2 * q + 1], yb, acc1[r]);
                     }
-                    {
-                        const ulonglong2 ws = *reinterpret_cast<const ulonglong2*>(&sm.wsm[warp][q][lane]);
-                        acc[SR] = ffma2(ws.x, xa, acc[SR]);
-                        acc[SR] = ffma2(ws.y, xb, acc[SR]);
+#pragma unroll
+                    for (int j = 0; j < NSR; ++j) {
+                        const ulonglong2 ws = *reinterpret_cast<const ulonglong2*>(&sm.wsm[warp][j][q][lane]);
+                        acc0[SR + j] = ffma2(ws.x, xa, acc0[SR + j]);
+                        acc1[SR + j] = ffma2(ws.x, ya, acc1[SR + j]);
+                        acc0[SR + j] = ffma2(ws.y, xb, acc0[SR + j]);
+                        acc1[SR + j] = ffma2(ws.y, yb, acc1[SR + j]);
                     }
                     tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
                     for (int t = 0; t < TR; ++t) {
-                        acc[RR + t] = ffma2(pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1])), xa, acc[RR + t]);
-                        acc[RR + t] = ffma2(pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3])), xb,
-                                            acc[RR + t]);
+                        const uint64_t wa = pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1]));
+                        const uint64_t wb = pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3]));
+                        acc0[RR + t] = ffma2(wa, xa, acc0[RR + t]);
+                        acc1[RR + t] = ffma2(wa, ya, acc1[RR + t]);
+                        acc0[RR + t] = ffma2(wb, xb, acc0[RR + t]);
+                        acc1[RR + t] = ffma2(wb, yb, acc1[RR + t]);
                     }
                 }
-                float px;
+                // tail: lane l holds row l >> 1, columns 768 + 8·(l & 1) .. +7; partials of both samples
+                float pt0, pt1;
                 {
                     uint32_t tt[8];
                     tmem::ld8(tq + TTAIL, tt);
-                    const float* xt = xring + sl * DP + XC + 8 * th8;
-                    const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
+                    const float* xt0 = xring + sl0 * DP + XC + 8 * th8;
+                    const float* xt1 = xring + sl1 * DP + XC + 8 * th8;
+                    const float4 a0 = *reinterpret_cast<const float4*>(xt0), a1 = *reinterpret_cast<const float4*>(xt0 + 4);
+                    const float4 c0 = *reinterpret_cast<const float4*>(xt1), c1 = *reinterpret_cast<const float4*>(xt1 + 4);
                     tmem::wait_ld_regs<8>(tt);
-                    px = __uint_as_float(tt[0]) * x0.x;
-                    px = fmaf(__uint_as_float(tt[1]), x0.y, px); px = fmaf(__uint_as_float(tt[2]), x0.z, px);
-                    px = fmaf(__uint_as_float(tt[3]), x0.w, px); px = fmaf(__uint_as_float(tt[4]), x1.x, px);
-                    px = fmaf(__uint_as_float(tt[5]), x1.y, px); px = fmaf(__uint_as_float(tt[6]), x1.z, px);
-                    px = fmaf(__uint_as_float(tt[7]), x1.w, px);
+                    const float wt[8] = {__uint_as_float(tt[0]), __uint_as_float(tt[1]), __uint_as_float(tt[2]),
+                                         __uint_as_float(tt[3]), __uint_as_float(tt[4]), __uint_as_float(tt[5]),
+                                         __uint_as_float(tt[6]), __uint_as_float(tt[7])};
+                    pt0 = wt[0] * a0.x;
+                    pt0 = fmaf(wt[1], a0.y, pt0); pt0 = fmaf(wt[2], a0.z, pt0); pt0 = fmaf(wt[3], a0.w, pt0);
+                    pt0 = fmaf(wt[4], a1.x, pt0); pt0 = fmaf(wt[5], a1.y, pt0); pt0 = fmaf(wt[6], a1.z, pt0);
+                    pt0 = fmaf(wt[7], a1.w, pt0);
+                    pt1 = wt[0] * c0.x;
+                    pt1 = fmaf(wt[1], c0.y, pt1); pt1 = fmaf(wt[2], c0.z, pt1); pt1 = fmaf(wt[3], c0.w, pt1);
+                    pt1 = fmaf(wt[4], c1.x, pt1); pt1 = fmaf(wt[5], c1.y, pt1); pt1 = fmaf(wt[6], c1.z, pt1);
+                    pt1 = fmaf(wt[7], c1.w, pt1);
                 }
-                float v[RPW];
+                // transpose-reduce 32 values v[2r + sample]: lane l ends with value l
+                float v[2 * RPW];
 #pragma unroll
                 for (int r = 0; r < RPW; ++r) {
                     float lo, hi;
-                    upk(acc[r], lo, hi);
-                    v[r] = lo + hi;
+                    upk(acc0[r], lo, hi);
+                    v[2 * r] = lo + hi;
+                    upk(acc1[r], lo, hi);
+                    v[2 * r + 1] = lo + hi;
                 }
-                float zsum = treduce16(v, lane) + px;
-                zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
-                if (th8 == 0) sm.asum[s % AR][kr0 + trow] = zsum;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.aready[s % AR]);
-            }
-            // ---------------- U(s-L): W¹ -= g(s-L)·x(s-L)ᵀ ----------------
-            const int uu = s - LAG;
-            if (uu >= 0 && uu < T) {
-                mbar_wait(&sm.gready[uu % GR], (uint32_t)((uu / GR) & 1));
-                const float* xo = xring + (uu % S) * DP + 4 * lane;
-                uint64_t gp[RPW];                   // (-g, -g) of each row
+                float zsum;
                 {
-                    const float4* gv = reinterpret_cast<const float4*>(&sm.gbuf[uu % GR][kr0]);
+                    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+                    float u16[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        u16[i] = (b4 ? v[i + 16] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 16], 16);
+                    float u8[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        u8[i] = (b3 ? u16[i + 8] : u16[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u16[i] : u16[i + 8], 8);
+                    float u4[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        u4[i] = (b2 ? u8[i + 4] : u8[i]) + __shfl_xor_sync(0xffffffffu, b2 ? u8[i] : u8[i + 4], 4);
+                    float u2[2];
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+                        u2[i] = (b1 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b1 ? u4[i] : u4[i + 2], 2);
+                    zsum = (b0 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b0 ? u2[0] : u2[1], 1);
+                    // + the tail of (row l >> 1, sample l & 1): this lane's half and the partner's
+                    const float other = __shfl_xor_sync(0xffffffffu, trs ? pt0 : pt1, 1);
+                    zsum += (trs ? pt1 : pt0) + other;
+                }
+                if (trs == 0 || v1) sm.asum[(trs ? s1 : s0) % AR][kr0 + (lane >> 1)] = zsum;
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm.aready[s0 % AR]);
+                    if (v1) mbar_arrive(&sm.aready[s1 % AR]);
+                }
+            }
+            // ---------------- U(2p-4), U(2p-3): W¹ -= g(u)·x(u)ᵀ in sample order ----------------
+            if (p >= 2 && 2 * (p - 2) < T) {
+                const int u0 = 2 * (p - 2), u1 = u0 + 1;
+                const bool v1 = u1 < T;
+                const int ul = v1 ? u1 : u0;            // chain u1 done ⇒ chain u0 done
+                mbar_wait(&sm.gready[ul % GR], (uint32_t)((ul / GR) & 1));
+                const int sl0 = u0 % S, sl1 = v1 ? u1 % S : S;
+                const float* xo0 = xring + sl0 * DP + 4 * lane;
+                const float* xo1 = xring + sl1 * DP + 4 * lane;
+                float gn0[RPW], gn1[RPW];               // -g of each row, samples u0, u1
+                {
+                    const float4* g0v = reinterpret_cast<const float4*>(&sm.gbuf[u0 % GR][kr0]);
+                    const float4* g1v = reinterpret_cast<const float4*>(&sm.gbuf[u1 % GR][kr0]);
 #pragma unroll
                     for (int i = 0; i < RPW / 4; ++i) {
-                        const float4 a = gv[i];
-                        gp[4 * i] = pk(-a.x, -a.x); gp[4 * i + 1] = pk(-a.y, -a.y);
-                        gp[4 * i + 2] = pk(-a.z, -a.z); gp[4 * i + 3] = pk(-a.w, -a.w);
+                        const float4 a = g0v[i];
+                        float4 b = g1v[i];
+                        if (!v1) b = make_float4(0.f, 0.f, 0.f, 0.f);
+                        gn0[4 * i] = -a.x; gn0[4 * i + 1] = -a.y; gn0[4 * i + 2] = -a.z; gn0[4 * i + 3] = -a.w;
+                        gn1[4 * i] = -b.x; gn1[4 * i + 1] = -b.y; gn1[4 * i + 2] = -b.z; gn1[4 * i + 3] = -b.w;
                     }
                 }
+#define GP0(r) pk(gn0[r], gn0[r])
+#define GP1(r) pk(gn1[r], gn1[r])
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
+                for (int q = 0; q < (PNN_WS_EXP == 1 ? 0 : NQ); ++q) {
                     uint32_t tv[TQCOLS];
                     tmem::ld32(tq + q * TQCOLS, tv);
                     tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
-                    uint64_t xa, xb;
-                    lds4(xo + 128 * q, xa, xb);
+                    uint64_t xa, xb, ya, yb;
+                    lds4(xo0 + 128 * q, xa, xb);
+                    lds4(xo1 + 128 * q, ya, yb);
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
-                        w[r][2 * q] = ffma2(gp[r], xa, w[r][2 * q]);
-                        w[r][2 * q + 1] = ffma2(gp[r], xb, w[r][2 * q + 1]);
+                        w[r][2 * q] = ffma2(GP1(r), ya, ffma2(GP0(r), xa, w[r][2 * q]));
+                        w[r][2 * q + 1] = ffma2(GP1(r), yb, ffma2(GP0(r), xb, w[r][2 * q + 1]));
                     }
-                    {
-                        ulonglong2* wp = reinterpret_cast<ulonglong2*>(&sm.wsm[warp][q][lane]);
+#pragma unroll
+                    for (int j = 0; j < NSR; ++j) {
+                        ulonglong2* wp = reinterpret_cast<ulonglong2*>(&sm.wsm[warp][j][q][lane]);
                         ulonglong2 ws = *wp;
-                        ws.x = ffma2(gp[SR], xa, ws.x);
-                        ws.y = ffma2(gp[SR], xb, ws.y);
+                        ws.x = ffma2(GP1(SR + j), ya, ffma2(GP0(SR + j), xa, ws.x));
+                        ws.y = ffma2(GP1(SR + j), yb, ffma2(GP0(SR + j), xb, ws.y));
                         *wp = ws;
                     }
                     tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
                     for (int t = 0; t < TR; ++t) {
-                        const uint64_t gg = gp[RR + t];
-                        const uint64_t a = ffma2(gg, xa, pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1])));
-                        const uint64_t b = ffma2(gg, xb, pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3])));
+                        const uint64_t a = ffma2(GP1(RR + t), ya, ffma2(GP0(RR + t), xa,
+                                                 pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1]))));
+                        const uint64_t b = ffma2(GP1(RR + t), yb, ffma2(GP0(RR + t), xb,
+                                                 pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3]))));
                         float a0, a1, b0, b1;
                         upk(a, a0, a1);
                         upk(b, b0, b1);
@@ -327,16 +409,23 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 {
                     uint32_t tt[8];
                     tmem::ld8(tq + TTAIL, tt);
-                    const float* xt = xring + (uu % S) * DP + XC + 8 * th8;
-                    const float4 x0 = *reinterpret_cast<const float4*>(xt), x1 = *reinterpret_cast<const float4*>(xt + 4);
-                    const float gt = -sm.gbuf[uu % GR][kr0 + trow];
+                    const float* xt0 = xring + sl0 * DP + XC + 8 * th8;
+                    const float* xt1 = xring + sl1 * DP + XC + 8 * th8;
+                    const float4 a0 = *reinterpret_cast<const float4*>(xt0), a1 = *reinterpret_cast<const float4*>(xt0 + 4);
+                    const float4 c0 = *reinterpret_cast<const float4*>(xt1), c1 = *reinterpret_cast<const float4*>(xt1 + 4);
+                    const float ga = -sm.gbuf[u0 % GR][kr0 + trow];
+                    const float gb = v1 ? -sm.gbuf[u1 % GR][kr0 + trow] : 0.f;
                     tmem::wait_ld_regs<8>(tt);
-                    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float yv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) tt[j] = __float_as_uint(fmaf(gt, xv[j], __uint_as_float(tt[j])));
+                    for (int j = 0; j < 8; ++j)
+                        tt[j] = __float_as_uint(fmaf(gb, yv[j], fmaf(ga, xv[j], __uint_as_float(tt[j]))));
                     tmem::st8(tq + TTAIL, tt);
                 }
                 tmem::wait_st();
+#undef GP0
+#undef GP1
             }
         }
 
@@ -365,11 +454,13 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 }
             }
         }
-        if (kr0 + SR < H) {
-            float* dst = opaque(W1) + (long long)(kr0 + SR) * D + 4 * lane;
+#pragma unroll
+        for (int j = 0; j < NSR; ++j) {
+            if (kr0 + SR + j >= H) continue;
+            float* dst = opaque(W1) + (long long)(kr0 + SR + j) * D + 4 * lane;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const float4 v4 = sm.wsm[warp][q][lane];
+                const float4 v4 = sm.wsm[warp][j][q][lane];
                 *reinterpret_cast<float2*>(dst + 128 * q) = make_float2(v4.x, v4.y);
                 *reinterpret_cast<float2*>(dst + 128 * q + 2) = make_float2(v4.z, v4.w);
             }
@@ -396,55 +487,107 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 #pragma unroll
         for (int o = 0; o < O; ++o) w2[o] = lc ? W2[(long long)o * H + u] : 0.f;
         float b1 = lc ? b1g[u] : 0.f;
-        float g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f;   // g(c-1) .. g(c-4) of this unit
+        float g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f;   // g(c-1) .. g(c-5) of this unit
+        const float4* Rc = rec + 2 * row0;
         auto issue_x = [&](int s) {
             uint64_t* bar = &sm.xfull[s % S];
-            mbar_arrive_expect_tx(bar, xbytes);
+            mbar_arrive_expect_tx(bar, xbytes + (PRE ? 32u : 0u));
             bulk_g2s(xring + (s % S) * DP, Xc + (long long)s * D, xbytes, bar);
+            if constexpr (PRE) bulk_g2s(xring + (s % S) * DP + GOFF, Rc + 2 * s, 32u, bar);
         };
         if (leader)
             for (int s = 0; s < PF && s < T; ++s) issue_x(s);
         int lab0 = (T > 0) ? __ldg(Yc) : 0;          // labels of samples c, c+1
         int lab1 = (T > 1) ? __ldg(Yc + 1) : 0;
-        const int gk = cw + 1;                      // this warp's Gram term: G(s-gk, s)
         for (int c = 0; c < T; ++c) {
-            const int lab2 = (c + 2 < T) ? __ldg(Yc + c + 2) : 0;
-            // ---- G(c+1-k, c+1), k = cw + 1, one sample ahead (R27) ----
-            if (c + 1 < T) {
-                const int s1 = c + 1;
-                mbar_wait(&sm.xfull[s1 % S], (uint32_t)((s1 / S) & 1));
-                const float* xa = xring + (s1 % S) * DP + 4 * lane;
-                const float* xb = xring + ((s1 - gk >= 0) ? (s1 - gk) % S : S) * DP + 4 * lane;
-                uint64_t ga = 0ull;
+            const int lab2 = (!PRE && c + 2 < T) ? __ldg(Yc + c + 2) : 0;
+            // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c), h(c) ----
+            if constexpr (PRE) mbar_wait(&sm.xfull[c % S], (uint32_t)((c / S) & 1));   // x(c)'s record
+            else if (c + 1 < T) mbar_wait(&sm.xfull[(c + 1) % S], (uint32_t)(((c + 1) / S) & 1));   // for G(·, c+1)
+            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
+            if constexpr (PNN_WS_EXP == 2) {
+                sm.gbuf[c % GR][u] = 0.f;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.gready[c % GR]);
+                if (leader && c + PF < T) issue_x(c + PF);
+                continue;
+            }
+            float G[5];                             // G(c-k, c), k = 1..5 (formed during chain c-1)
+            if constexpr (PRE) {                    // {G(c-4), G(c-3), G(c-2), G(c-1)}, {label, G(c-5)}
+                const float4 r0 = *reinterpret_cast<const float4*>(xring + (c % S) * DP + GOFF);
+                const float2 r1 = *reinterpret_cast<const float2*>(xring + (c % S) * DP + GOFF + 4);
+                G[0] = r0.w; G[1] = r0.z; G[2] = r0.y; G[3] = r0.x; G[4] = r1.y;
+                lab0 = __float_as_int(r1.x);
+            } else {
+                const float4 g4v = *reinterpret_cast<const float4*>(&sm.gpart[c % GT][0]);
+                const float4 g5v = *reinterpret_cast<const float4*>(&sm.gpart[c % GT][4]);
+                G[0] = g4v.x; G[1] = g4v.y; G[2] = g4v.z; G[3] = g4v.w;
+                G[4] = (g5v.x + g5v.y) + (g5v.z + g5v.w);
+            }
+            float z = sm.asum[c % AR][u];
+            if (c & 1) z = fmaf(-g5, G[4], z);
+            z = fmaf(-g4, G[3], z);
+            z = fmaf(-g3, G[2], z);
+            z = fmaf(-g2, G[1], z);
+            z = fmaf(-g1, G[0], z);
+            z += b1;
+            const float h = lc ? act_fwd_t<A1>(z) : 0.f;
+            if constexpr (!PRE)
+            // ---- G(c+1-k, c+1): term k = cw + 1 over all columns, and a quarter of the k = 5 term
+            //      (odd samples; the paired sweeps' odd samples miss 5 updates), branch-free so the
+            //      compiler interleaves it with the partial logits below (R27) ----
+            {
+                const int s1 = c + 1;                   // (s1 = T: any slot; nothing is stored)
+                const float* xa = xring + (s1 % S) * DP;
+                const float* xb = xring + ((s1 - 1 - cw >= 0) ? (s1 - 1 - cw) % S : S) * DP;
+                const float* xc = xring + ((s1 - 5 >= 0) ? (s1 - 5) % S : S) * DP;
+                uint64_t ga = 0ull, gc = 0ull;
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
                     uint64_t a0, a1, b0, b1v;
-                    lds4(xa + 128 * q, a0, a1);
-                    lds4(xb + 128 * q, b0, b1v);
+                    lds4(xa + 4 * lane + 128 * q, a0, a1);
+                    lds4(xb + 4 * lane + 128 * q, b0, b1v);
                     ga = ffma2(a0, b0, ga);
                     ga = ffma2(a1, b1v, ga);
                 }
-                float glo, ghi;
-                upk(ga, glo, ghi);
-                float g = glo + ghi;
-                if (lane < 4) {                         // columns 768 + 4·lane .. +3 (zero past D)
-                    const float4 a = *reinterpret_cast<const float4*>(xa - 4 * lane + XC + 4 * lane);
-                    const float4 b = *reinterpret_cast<const float4*>(xb - 4 * lane + XC + 4 * lane);
-                    g = fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, fmaf(a.x, b.x, g))));
+                // k = 5: warp cw takes quads cw and cw + 4 (warps 2, 3: quad cw only; warp 3 the tail)
+                uint64_t gc2 = 0ull;
+                {
+                    const int qb = (cw + 4 < NQ) ? cw + 4 : cw;
+                    uint64_t a0, a1, c0, c1;
+                    lds4(xa + 4 * lane + 128 * cw, a0, a1);
+                    lds4(xc + 4 * lane + 128 * cw, c0, c1);
+                    gc = ffma2(a1, c1, ffma2(a0, c0, gc));
+                    lds4(xa + 4 * lane + 128 * qb, a0, a1);
+                    lds4(xc + 4 * lane + 128 * qb, c0, c1);
+                    gc2 = ffma2(a1, c1, ffma2(a0, c0, gc2));
                 }
-                g = warp_sum(g);
-                if (lane == 0) sm.gterm[s1 % GT][cw] = g;
+                float lo, hi;
+                upk(ga, lo, hi);
+                float gv = lo + hi;
+                upk(gc, lo, hi);
+                float gw = lo + hi;
+                upk(gc2, lo, hi);
+                gw += (cw + 4 < NQ) ? lo + hi : 0.f;
+                {                                       // columns 768 + 4·(lane & 3) .. +3 (zero past D)
+                    const float4 a = *reinterpret_cast<const float4*>(xa + XC + 4 * (lane & 3));
+                    const float4 b = *reinterpret_cast<const float4*>(xb + XC + 4 * (lane & 3));
+                    const float4 e = *reinterpret_cast<const float4*>(xc + XC + 4 * (lane & 3));
+                    const float tb = fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
+                    const float te = fmaf(a.w, e.w, fmaf(a.z, e.z, fmaf(a.y, e.y, a.x * e.x)));
+                    gv += (lane < 4) ? tb : 0.f;
+                    gw += (lane < 4 && cw == 3) ? te : 0.f;
+                }
+                // lanes < 16 end with Σ gv, lanes >= 16 with Σ gw
+                const bool hi16 = lane & 16;
+                float gg = (hi16 ? gw : gv) + __shfl_xor_sync(0xffffffffu, hi16 ? gv : gw, 16);
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) gg += __shfl_xor_sync(0xffffffffu, gg, o);
+                if (s1 < T) {
+                    if (lane == 0) sm.gpart[s1 % GT][cw] = gg;
+                    if (lane == 16) sm.gpart[s1 % GT][4 + cw] = gg;
+                }
             }
-            // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c), h(c) ----
-            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
-            const float4 G = *reinterpret_cast<const float4*>(&sm.gterm[c % GT][0]);   // k = 1..4
-            float z = sm.asum[c % AR][u];
-            z = fmaf(-g4, G.w, z);
-            z = fmaf(-g3, G.z, z);
-            z = fmaf(-g2, G.y, z);
-            z = fmaf(-g1, G.x, z);
-            z += b1;
-            const float h = lc ? act_fwd_t<A1>(z) : 0.f;
             // ---- this warp's partial logits Σ_u W2[o][u] h_u ----
             {
                 float pv[16];
@@ -507,7 +650,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
             b1 -= gu;
 #pragma unroll
             for (int o = 0; o < O; ++o) w2[o] = fmaf(-(lr * dl[o]), h, w2[o]);
-            g4 = g3; g3 = g2; g2 = g1; g1 = gu;
+            g5 = g4; g4 = g3; g3 = g2; g2 = g1; g1 = gu;
             if (leader) {
                 // b2(c+1) into the other buffer (the other threads may still read b2(c))
                 const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);
@@ -542,13 +685,13 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 }
 
 template <int A1, int A2>
-cudaError_t launch_one(const NetDesc& d, float* children, const float* x, const int32_t* y, long long n_local,
-                       int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
-    auto kern = sgd_ws_kernel<A1, A2>;
+cudaError_t launch_one(const NetDesc& d, float* children, const float* x, const int32_t* y, const float4* rec,
+                       long long n_local, int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
+    auto kern = rec ? sgd_ws_kernel<A1, A2, true> : sgd_ws_kernel<A1, A2, false>;
     const size_t smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<s_count, NT, smem, st>>>(d, children, x, y, n_local, K_local, s_first, lr);
+    kern<<<s_count, NT, smem, st>>>(d, children, x, y, rec, n_local, K_local, s_first, lr);
     return cudaGetLastError();
 }
 
@@ -571,11 +714,11 @@ const char* ws_plan(const NetDesc& d, int batch) {
     return nullptr;
 }
 
-cudaError_t launch_sgd_ws(const NetDesc& d, float* children, const float* x, const int32_t* y, long long n_local,
-                          int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
+cudaError_t launch_sgd_ws(const NetDesc& d, float* children, const float* x, const int32_t* y, const float4* rec,
+                          long long n_local, int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
     if (s_count <= 0) return cudaSuccess;
 #define PNN_ACTS(A1_, A2_) \
-    if (d.act[0] == A1_ && d.act[1] == A2_) return launch_one<A1_, A2_>(d, children, x, y, n_local, K_local, s_first, s_count, lr, st);
+    if (d.act[0] == A1_ && d.act[1] == A2_) return launch_one<A1_, A2_>(d, children, x, y, rec, n_local, K_local, s_first, s_count, lr, st);
     PNN_ACTS(PNN_RELU, PNN_SOFTMAX)
     PNN_ACTS(PNN_TANH, PNN_SOFTMAX)
     PNN_ACTS(PNN_SIGMOID, PNN_SOFTMAX)

@@ -13,6 +13,8 @@ rows = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 X, y = make_rows(0, K * rows, "train", 0)
 net = PNN(c.layers, c.act, c.init, K, c.lr, seed=0)
 net.set_kernel("resident")
+if len(sys.argv) > 3:
+    net.set_variant(sys.argv[3])
 xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
 net.train_epoch(xd, yd)
 torch.cuda.synchronize()
