@@ -36,6 +36,13 @@
 #ifndef PNN_WS_EXP
 #define PNN_WS_EXP 0   // experiment builds only: 1 = sweeps without FMAs, 2 = chain without compute
 #endif
+#ifdef PNN_WS_TRACE
+// experiment builds only: clock64 timeline of CTA 0 (tools/trace_ws.py): [i < 256][point < 8]
+#define WS_TR(i, pt) do { if (trace && blockIdx.x == 0 && lane == 0 && (i) < 256) trace[(i) * 8 + (pt)] = ptx::clock64(); } while (0)
+#else
+#define WS_TR(i, pt) do { } while (0)
+#endif
+extern long long* g_trace;   // debug: clock64 timeline (k_resident.cu; tools/trace_ws.py, PNN_WS_TRACE builds)
 namespace {
 
 using namespace ptx;
@@ -144,7 +151,8 @@ __device__ __forceinline__ float treduce16(const float (&v)[16], int lane) {
 template <int A1, int A2, bool PRE>
 __global__ void __launch_bounds__(NT, 1)
 sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ X, const int32_t* __restrict__ Y,
-              const float4* __restrict__ rec, long long n_local, int K_local, int s_first, float lr) {
+              const float4* __restrict__ rec, long long n_local, int K_local, int s_first, float lr,
+              long long* __restrict__ trace) {
     extern __shared__ __align__(128) unsigned char smraw[];
     Smem& sm = *reinterpret_cast<Smem*>(smraw);
     float* xring = reinterpret_cast<float*>(smraw + kSmemHead);
@@ -236,13 +244,14 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
         const int npair = (T + 1) >> 1;
         const int trs = lane & 1;                       // F's reduce: lane l ends with (row l >> 1, sample l & 1)
         for (int p = 0; p < npair + 2; ++p) {
+            if (warp == 0) WS_TR(p, 4);
             if (p < npair) {
                 // ---------------- F(2p), F(2p+1): acc = W¹(2p-4)·x ----------------
                 const int s0 = 2 * p, s1 = s0 + 1;
                 const bool v1 = s1 < T;
                 const int sl0 = s0 % S, sl1 = v1 ? s1 % S : S;   // slot S: the zero row
-                mbar_wait(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
-                if (v1) mbar_wait(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
+                mbar_wait_sleep(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
+                if (v1) mbar_wait_sleep(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
                 const float* xn0 = xring + sl0 * DP + 4 * lane;
                 const float* xn1 = xring + sl1 * DP + 4 * lane;
                 uint64_t acc0[RPW], acc1[RPW];
@@ -344,13 +353,15 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                     mbar_arrive(&sm.aready[s0 % AR]);
                     if (v1) mbar_arrive(&sm.aready[s1 % AR]);
                 }
+                if (warp == 0) WS_TR(p, 5);
             }
             // ---------------- U(2p-4), U(2p-3): W¹ -= g(u)·x(u)ᵀ in sample order ----------------
             if (p >= 2 && 2 * (p - 2) < T) {
                 const int u0 = 2 * (p - 2), u1 = u0 + 1;
                 const bool v1 = u1 < T;
                 const int ul = v1 ? u1 : u0;            // chain u1 done ⇒ chain u0 done
-                mbar_wait(&sm.gready[ul % GR], (uint32_t)((ul / GR) & 1));
+                mbar_wait_sleep(&sm.gready[ul % GR], (uint32_t)((ul / GR) & 1));
+                if (warp == 0) WS_TR(p, 6);
                 const int sl0 = u0 % S, sl1 = v1 ? u1 % S : S;
                 const float* xo0 = xring + sl0 * DP + 4 * lane;
                 const float* xo1 = xring + sl1 * DP + 4 * lane;
@@ -384,11 +395,10 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                     }
 #pragma unroll
                     for (int j = 0; j < NSR; ++j) {
-                        ulonglong2* wp = reinterpret_cast<ulonglong2*>(&sm.wsm[warp][j][q][lane]);
-                        ulonglong2 ws = *wp;
-                        ws.x = ffma2(GP1(SR + j), ya, ffma2(GP0(SR + j), xa, ws.x));
-                        ws.y = ffma2(GP1(SR + j), yb, ffma2(GP0(SR + j), xb, ws.y));
-                        *wp = ws;
+                        uint64_t* wp = reinterpret_cast<uint64_t*>(&sm.wsm[warp][j][q][lane]);
+                        const ulonglong2 ws = *reinterpret_cast<const ulonglong2*>(wp);
+                        wp[0] = ffma2(GP1(SR + j), ya, ffma2(GP0(SR + j), xa, ws.x));   // two 8-byte stores:
+                        wp[1] = ffma2(GP1(SR + j), yb, ffma2(GP0(SR + j), xb, ws.y));   // no re-pack MOVs
                     }
                     tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
@@ -424,6 +434,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                     tmem::st8(tq + TTAIL, tt);
                 }
                 tmem::wait_st();
+                if (warp == 0) WS_TR(p, 7);
 #undef GP0
 #undef GP1
             }
@@ -502,9 +513,11 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
         for (int c = 0; c < T; ++c) {
             const int lab2 = (!PRE && c + 2 < T) ? __ldg(Yc + c + 2) : 0;
             // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c), h(c) ----
-            if constexpr (PRE) mbar_wait(&sm.xfull[c % S], (uint32_t)((c / S) & 1));   // x(c)'s record
-            else if (c + 1 < T) mbar_wait(&sm.xfull[(c + 1) % S], (uint32_t)(((c + 1) / S) & 1));   // for G(·, c+1)
-            mbar_wait(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
+            if (cw == 0) WS_TR(c, 0);
+            if constexpr (PRE) mbar_wait_sleep(&sm.xfull[c % S], (uint32_t)((c / S) & 1));   // x(c)'s record
+            else if (c + 1 < T) mbar_wait_sleep(&sm.xfull[(c + 1) % S], (uint32_t)(((c + 1) / S) & 1));   // for G(·, c+1)
+            mbar_wait_sleep(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
+            if (cw == 0) WS_TR(c, 1);
             if constexpr (PNN_WS_EXP == 2) {
                 sm.gbuf[c % GR][u] = 0.f;
                 __syncwarp();
@@ -598,46 +611,36 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 if ((lane & 1) == 0 && (lane >> 1) < O) sm.zp[c & 1][cw][lane >> 1] = p0;
             }
             named_bar_sync(1, 32 * NCW);            // the four warps' partials of sample c
-            // ---- δ2(c) in every thread ----
+            if (cw == 0) WS_TR(c, 2);
+            // ---- δ2(c): lane o < 10 of every chain warp forms z2_o and its share of the softmax /
+            //      φ2, then every lane takes the ten δ2 by shuffles ----
             float dl[O];
+            const int ol = lane < O ? lane : 0;
+            const float b2o = sm.b2s[c & 1][ol];    // b2(c)_o
             {
-                float z2[O];
-                const float4* a = reinterpret_cast<const float4*>(&sm.zp[c & 1][0][0]);
-                const float4* b = reinterpret_cast<const float4*>(&sm.zp[c & 1][1][0]);
-                const float4* e = reinterpret_cast<const float4*>(&sm.zp[c & 1][2][0]);
-                const float4* f = reinterpret_cast<const float4*>(&sm.zp[c & 1][3][0]);
-                const float4* bb = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const float4 x = a[q], y = b[q], v = e[q], t = f[q], bq = bb[q];
-                    const float t4[4] = {((x.x + y.x) + (v.x + t.x)) + bq.x, ((x.y + y.y) + (v.y + t.y)) + bq.y,
-                                         ((x.z + y.z) + (v.z + t.z)) + bq.z, ((x.w + y.w) + (v.w + t.w)) + bq.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (4 * q + i < O) z2[4 * q + i] = t4[i];   // z2 = W2 h + b2 (Eq.2)
-                }
+                const float z2 = ((sm.zp[c & 1][0][ol] + sm.zp[c & 1][1][ol]) +
+                                  (sm.zp[c & 1][2][ol] + sm.zp[c & 1][3][ol])) + b2o;   // z2 = W2 h + b2 (Eq.2)
+                float dmine;
                 if constexpr (A2 == PNN_SOFTMAX) {
-                    const float m = fmaxf(fmaxf(fmaxf(z2[0], z2[1]), fmaxf(z2[2], z2[3])),
-                                          fmaxf(fmaxf(fmaxf(z2[4], z2[5]), fmaxf(z2[6], z2[7])), fmaxf(z2[8], z2[9])));
+                    float m = lane < O ? z2 : -INFINITY;
 #pragma unroll
-                    for (int o = 0; o < O; ++o) dl[o] = __expf(z2[o] - m);
-                    const float sum = ((dl[0] + dl[1]) + (dl[2] + dl[3])) +
-                                      (((dl[4] + dl[5]) + (dl[6] + dl[7])) + (dl[8] + dl[9]));
+                    for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    const float ez = lane < O ? __expf(z2 - m) : 0.f;
+                    float sum = ez;
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
                     float inv;
                     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(sum));
-#pragma unroll
-                    for (int o = 0; o < O; ++o) dl[o] = dl[o] * inv - ((o == lab0) ? 1.f : 0.f);
+                    dmine = ez * inv - ((lane == lab0) ? 1.f : 0.f);
                 } else {
-                    // element-wise output (sigmoid / tanh, ½-SSE: Eq.9, R11): lane o forms output
-                    // o's activation and δ2 once, then every lane takes the ten by shuffles
-                    float zsel = z2[0];
-#pragma unroll
-                    for (int o = 1; o < O; ++o) zsel = (lane == o) ? z2[o] : zsel;
-                    const float x2 = act_fwd_t<A2>(zsel);
-                    const float dmine = (x2 - ((lane == lab0) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
-#pragma unroll
-                    for (int o = 0; o < O; ++o) dl[o] = __shfl_sync(0xffffffffu, dmine, o);
+                    // element-wise output (sigmoid / tanh, ½-SSE: Eq.9, R11)
+                    const float x2 = act_fwd_t<A2>(z2);
+                    dmine = (x2 - ((lane == lab0) ? 1.f : 0.f)) * act_deriv_t<A2>(x2);
                 }
+#pragma unroll
+                for (int o = 0; o < O; ++o) dl[o] = __shfl_sync(0xffffffffu, dmine, o);
+                // b2(c+1) into the other buffer (the other warps may still read b2(c)): warp 0, lanes < 10
+                if (cw == 0 && lane < O) sm.b2s[(c + 1) & 1][lane] = fmaf(-lr, dmine, b2o);
             }
             // ---- δ1, g(c) → the sweeps; W2, b1, b2 updates ----
             float s1 = 0.f;                         // (W2ᵀδ2)_u with the pre-update W2 (R6)
@@ -647,20 +650,12 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
             sm.gbuf[c % GR][u] = gu;
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.gready[c % GR]);
+            if (cw == 0) WS_TR(c, 3);
             b1 -= gu;
 #pragma unroll
             for (int o = 0; o < O; ++o) w2[o] = fmaf(-(lr * dl[o]), h, w2[o]);
             g5 = g4; g4 = g3; g3 = g2; g2 = g1; g1 = gu;
             if (leader) {
-                // b2(c+1) into the other buffer (the other threads may still read b2(c))
-                const float4* bo = reinterpret_cast<const float4*>(&sm.b2s[c & 1][0]);
-                float4* bq = reinterpret_cast<float4*>(&sm.b2s[(c + 1) & 1][0]);
-                const float4 a = bo[0], b = bo[1], e = bo[2];
-                bq[0] = make_float4(fmaf(-lr, dl[0], a.x), fmaf(-lr, dl[1], a.y), fmaf(-lr, dl[2], a.z),
-                                    fmaf(-lr, dl[3], a.w));
-                bq[1] = make_float4(fmaf(-lr, dl[4], b.x), fmaf(-lr, dl[5], b.y), fmaf(-lr, dl[6], b.z),
-                                    fmaf(-lr, dl[7], b.w));
-                bq[2] = make_float4(fmaf(-lr, dl[8], e.x), fmaf(-lr, dl[9], e.y), 0.f, 0.f);
                 // every sweep warp passed U(c-1-L) (aready(c)) and every chain warp is past its
                 // Gram read of x(c-3): the slot of x(c+PF-S) is free
                 if (c + PF < T) issue_x(c + PF);
@@ -691,7 +686,7 @@ cudaError_t launch_one(const NetDesc& d, float* children, const float* x, const 
     const size_t smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<s_count, NT, smem, st>>>(d, children, x, y, rec, n_local, K_local, s_first, lr);
+    kern<<<s_count, NT, smem, st>>>(d, children, x, y, rec, n_local, K_local, s_first, lr, g_trace);
     return cudaGetLastError();
 }
 

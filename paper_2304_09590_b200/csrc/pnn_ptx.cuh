@@ -51,6 +51,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
 }
 #endif
+// try_wait with a suspend-time hint: a waiter that is early sleeps (the hardware wakes it when the
+// phase completes) instead of spinning through issue slots its SM's other warps could use.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 // Non-suspending poll (test_wait) — for waiters whose wake-up latency is on the critical path.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
     asm volatile(
