@@ -1153,6 +1153,7 @@ ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int vari
     int v = variant;
     if (v == PNN_VARIANT_AUTO) {
         if (v10_ok && concurrent > 0 && (long long)concurrent * c10 <= 120) v = PNN_VARIANT_RESIDENT_V10;
+        else if (ws_plan(d, batch) == nullptr) v = PNN_VARIANT_RESIDENT_WS;   // v12: C4 83 M vs v11 67 M samples/s
         else if (tm_ok) v = PNN_VARIANT_RESIDENT_TMEM;
         else v = PNN_VARIANT_RESIDENT_V8;
     }
