@@ -380,8 +380,8 @@ def main():
                                    "registers + tensor memory, Gram terms formed in the launch)"
                                    if variant_id == 11 else
                                    "persistent SGD launch, warp-specialised TMEM variant (k_ws.cu: one SM per CN, "
-                                   "W1 in registers + tensor memory + shared memory, the per-sample chain on its own "
-                                   "warpgroup, Gram terms formed in the launch)"
+                                   "W1 in registers + tensor memory + shared memory, paired sweeps on 8 warps, the "
+                                   "per-sample chain on its own warpgroup; frac_epoch adds the Gram pre-pass)"
                                    if variant_id == 12 else
                                    "persistent SGD launch (library CUDA events around it; frac_epoch adds the "
                                    "Gram pre-pass)"),
