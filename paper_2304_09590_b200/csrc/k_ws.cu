@@ -50,17 +50,14 @@ using namespace ptx;
 constexpr int NSW = 8;          // sweep warps (warpgroups 0, 1)
 constexpr int NCW = 4;          // chain warps (warpgroup 2)
 constexpr int NT = 32 * (NSW + NCW);
-#ifndef PNN_WS_SMEM_ROWS
-#define PNN_WS_SMEM_ROWS 3
-#endif
-constexpr int NSR = PNN_WS_SMEM_ROWS;   // W¹ rows per sweep warp in shared memory (its last rows)
-constexpr int TR = 10;          // W¹ rows per sweep warp in TMEM
-constexpr int RR = 6 - NSR;     // W¹ rows per sweep warp in registers
-constexpr int SR = RR + TR;     // the warp's first row in shared memory
-constexpr int RPW = RR + TR + NSR;  // rows per sweep warp (16)
+constexpr int RPW = 16;         // W¹ rows per sweep warp (8 per half-warp)
+constexpr int RW = 8;           // rows per lane (its half-warp's)
+constexpr int RR = 3;           // of which in registers
+constexpr int TRW = RW - RR;    // and in TMEM
 constexpr int UMAX = NSW * RPW; // 128 hidden units
-constexpr int NQ = 6;           // column quads per lane: columns [0, 768)
+constexpr int NQ = 12;          // column quads per lane (4 columns each, stride 64): columns [0, 768)
 constexpr int NP = 2 * NQ;      // f32x2 pairs per lane per row
+constexpr int NQG = 6;          // the chain's Gram dot products: quads of 32 lanes x 4 columns (stride 128)
 constexpr int XC = 768;         // first tail column
 constexpr int DP = 800;         // x ring slot stride (floats)
 constexpr int GOFF = 784;       // PRE: the Gram record of x(u) at its slot + GOFF
@@ -71,7 +68,7 @@ constexpr int O = 10;           // outputs
 constexpr int AR = 8;           // row-sum ring slots (> L)
 constexpr int GR = 8;           // g ring slots (> L)
 constexpr int GT = 8;           // Gram-term ring slots (> L)
-constexpr int TQCOLS = 4 * TR;  // TMEM columns per quad
+constexpr int TQCOLS = 4 * TRW; // TMEM columns per quad
 constexpr int TTAIL = NQ * TQCOLS;
 // Register budgets per thread.  The launch gives every thread 168 (384 threads, one CTA per
 // SM); setmaxnreg moves them between warpgroups: 2·kSweepRegs + kChainRegs <= 3·168.
@@ -96,7 +93,6 @@ struct __align__(16) Smem {
     float zp[2][NCW][16];       // [c & 1][chain warp][o] partial logits
     float gpart[GT][8];         // [s % GT][j] j < 4: G(s-1-j, s); 4 + w: chain warp w's quarter of G(s-5, s)
     float b2s[2][12];           // b2 before sample c at [c & 1]
-    float4 wsm[NSW][NSR][NQ][32];   // [warp][row - SR][quad][lane] columns 4·lane + 128·quad .. +3
 };
 constexpr size_t kSmemHead = ((sizeof(Smem) + 127) / 128) * 128;
 
@@ -118,7 +114,6 @@ __device__ __forceinline__ void lds4(const float* p, uint64_t& a, uint64_t& b) {
     a = v.x;
     b = v.y;
 }
-__device__ __forceinline__ int pcol(int l, int j) { return 4 * l + 128 * (j >> 1) + 2 * (j & 1); }
 template <typename T> __device__ __forceinline__ T* opaque(T* p) {
     asm volatile("mov.b64 %0, %0;" : "+l"(p));
     return p;
@@ -188,49 +183,49 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 
     if (warp < NSW) {
         // ============================== sweep warps ==============================
+        // Half-warp layout: lanes 16·hw .. 16·hw+15 (hw = lane >> 4) hold rows kr0 + 8·hw .. +7 of
+        // the warp's 16, lane j = lane & 15 the 48 columns 4j + 64q .. +3 (q < 12) of each: RR rows
+        // in registers (f32x2 pairs), TRW in TMEM (20 columns per quad), the 16-column tail in TMEM
+        // (lane: row 8·hw + (j >> 1), columns 768 + 8·(j & 1) .. +7).  A row's dot product then sums
+        // over 16 lanes (a 16-value transpose-reduce per pair of samples) instead of 32.
         setmaxnreg_inc<kSweepRegs>();
         const uint32_t tq = sm.tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2);
-        const int kr0 = warp * RPW;
+        const int hw = lane >> 4, jl = lane & 15;
+        const int kr0 = warp * RPW;                     // the warp's first row
+        const int kh = kr0 + RW * hw;                   // this lane's first row
+        const int cl = 4 * jl;                          // this lane's first column
         uint64_t w[RR][NP];
 #pragma unroll
         for (int r = 0; r < RR; ++r) {
-            const bool live = kr0 + r < H;
-            const float* src = W1 + (long long)(kr0 + r) * D;
+            const bool live = kh + r < H;
+            const float* src = W1 + (long long)(kh + r) * D + cl;
 #pragma unroll
-            for (int m = 0; m < NP; ++m) w[r][m] = live ? *reinterpret_cast<const uint64_t*>(src + pcol(lane, m)) : 0ull;
+            for (int q = 0; q < NQ; ++q) {
+                w[r][2 * q] = live ? *reinterpret_cast<const uint64_t*>(src + 64 * q) : 0ull;
+                w[r][2 * q + 1] = live ? *reinterpret_cast<const uint64_t*>(src + 64 * q + 2) : 0ull;
+            }
         }
 #pragma unroll 1
         for (int q = 0; q < NQ; ++q) {
             uint32_t tv[TQCOLS];
 #pragma unroll
-            for (int t = 0; t < TR; ++t) {
-                const bool live = kr0 + RR + t < H;
-                const float* src = W1 + (long long)(kr0 + RR + t) * D + 4 * lane + 128 * q;
+            for (int t = 0; t < TRW; ++t) {
+                const bool live = kh + RR + t < H;
+                const float* src = W1 + (long long)(kh + RR + t) * D + cl + 64 * q;
                 // (slabs are 8-byte aligned only: P is even, not a multiple of 4)
                 const float2 a = live ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
                 const float2 b = live ? *reinterpret_cast<const float2*>(src + 2) : make_float2(0.f, 0.f);
                 tv[4 * t] = __float_as_uint(a.x); tv[4 * t + 1] = __float_as_uint(a.y);
                 tv[4 * t + 2] = __float_as_uint(b.x); tv[4 * t + 3] = __float_as_uint(b.y);
             }
-            tmem::st32(tq + q * TQCOLS, tv);
-            tmem::st8(tq + q * TQCOLS + 32, tv + 32);
+            tmem::st16(tq + q * TQCOLS, tv);
+            tmem::st4(tq + q * TQCOLS + 16, tv + 16);
         }
-#pragma unroll
-        for (int j = 0; j < NSR; ++j) {
-            const bool live = kr0 + SR + j < H;
-            const float* src = W1 + (long long)(kr0 + SR + j) * D + 4 * lane;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const float2 a = live ? *reinterpret_cast<const float2*>(src + 128 * q) : make_float2(0.f, 0.f);
-                const float2 b = live ? *reinterpret_cast<const float2*>(src + 128 * q + 2) : make_float2(0.f, 0.f);
-                sm.wsm[warp][j][q][lane] = make_float4(a.x, a.y, b.x, b.y);
-            }
-        }
-        const int trow = lane >> 1, th8 = lane & 1;     // tail: row kr0 + trow, columns 768 + 8·th8 .. +7
+        const int trow = kh + (jl >> 1), th8 = jl & 1;  // tail: row trow, columns 768 + 8·th8 .. +7
         {
             uint32_t tt[8];
-            const bool live = kr0 + trow < H;
-            const float* src = W1 + (long long)(kr0 + trow) * D + XC + 8 * th8;
+            const bool live = trow < H;
+            const float* src = W1 + (long long)trow * D + XC + 8 * th8;
 #pragma unroll
             for (int j = 0; j < 8; ++j) tt[j] = __float_as_uint((live && XC + 8 * th8 + j < D) ? src[j] : 0.f);
             tmem::st8(tq + TTAIL, tt);
@@ -242,7 +237,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
         // F(2p), F(2p+1) see W¹(2p-4): sample 2p misses 4 updates, 2p+1 misses 5 (R27; the chain
         // applies 4 / 5 Gram corrections).
         const int npair = (T + 1) >> 1;
-        const int trs = lane & 1;                       // F's reduce: lane l ends with (row l >> 1, sample l & 1)
+        const int trs = lane & 1;                       // F's reduce: lane ends with (row kh + (jl >> 1), sample lane & 1)
         for (int p = 0; p < npair + 2; ++p) {
             if (warp == 0) WS_TR(p, 4);
             if (p < npair) {
@@ -252,19 +247,19 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 const int sl0 = s0 % S, sl1 = v1 ? s1 % S : S;   // slot S: the zero row
                 mbar_wait_sleep(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
                 if (v1) mbar_wait_sleep(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
-                const float* xn0 = xring + sl0 * DP + 4 * lane;
-                const float* xn1 = xring + sl1 * DP + 4 * lane;
-                uint64_t acc0[RPW], acc1[RPW];
+                const float* xn0 = xring + sl0 * DP + cl;
+                const float* xn1 = xring + sl1 * DP + cl;
+                uint64_t acc0[RW], acc1[RW];
 #pragma unroll
-                for (int r = 0; r < RPW; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
+                for (int r = 0; r < RW; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
 #pragma unroll
                 for (int q = 0; q < (PNN_WS_EXP == 1 ? 0 : NQ); ++q) {
                     uint32_t tv[TQCOLS];
-                    tmem::ld32(tq + q * TQCOLS, tv);
-                    tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
+                    tmem::ld16(tq + q * TQCOLS, tv);
+                    tmem::ld4(tq + q * TQCOLS + 16, tv + 16);
                     uint64_t xa, xb, ya, yb;
-                    lds4(xn0 + 128 * q, xa, xb);
-                    lds4(xn1 + 128 * q, ya, yb);
+                    lds4(xn0 + 64 * q, xa, xb);
+                    lds4(xn1 + 64 * q, ya, yb);
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
                         acc0[r] = ffma2(w[r][2 * q], xa, acc0[r]);
@@ -272,17 +267,9 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                         acc0[r] = ffma2(w[r][2 * q + 1], xb, acc0[r]);
                         acc1[r] = ffma2(w[r][2 * q + 1], yb, acc1[r]);
                     }
-#pragma unroll
-                    for (int j = 0; j < NSR; ++j) {
-                        const ulonglong2 ws = *reinterpret_cast<const ulonglong2*>(&sm.wsm[warp][j][q][lane]);
-                        acc0[SR + j] = ffma2(ws.x, xa, acc0[SR + j]);
-                        acc1[SR + j] = ffma2(ws.x, ya, acc1[SR + j]);
-                        acc0[SR + j] = ffma2(ws.y, xb, acc0[SR + j]);
-                        acc1[SR + j] = ffma2(ws.y, yb, acc1[SR + j]);
-                    }
                     tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
-                    for (int t = 0; t < TR; ++t) {
+                    for (int t = 0; t < TRW; ++t) {
                         const uint64_t wa = pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1]));
                         const uint64_t wb = pk(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3]));
                         acc0[RR + t] = ffma2(wa, xa, acc0[RR + t]);
@@ -291,7 +278,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                         acc1[RR + t] = ffma2(wb, yb, acc1[RR + t]);
                     }
                 }
-                // tail: lane l holds row l >> 1, columns 768 + 8·(l & 1) .. +7; partials of both samples
+                // tail partials of both samples (row trow, 8 columns)
                 float pt0, pt1;
                 {
                     uint32_t tt[8];
@@ -313,10 +300,10 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                     pt1 = fmaf(wt[4], c1.x, pt1); pt1 = fmaf(wt[5], c1.y, pt1); pt1 = fmaf(wt[6], c1.z, pt1);
                     pt1 = fmaf(wt[7], c1.w, pt1);
                 }
-                // transpose-reduce 32 values v[2r + sample]: lane l ends with value l
-                float v[2 * RPW];
+                // transpose-reduce 16 values v[2r + sample] over the half-warp: lane jl ends with value jl
+                float v[2 * RW];
 #pragma unroll
-                for (int r = 0; r < RPW; ++r) {
+                for (int r = 0; r < RW; ++r) {
                     float lo, hi;
                     upk(acc0[r], lo, hi);
                     v[2 * r] = lo + hi;
@@ -325,15 +312,11 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 }
                 float zsum;
                 {
-                    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
-                    float u16[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        u16[i] = (b4 ? v[i + 16] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 16], 16);
+                    const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
                     float u8[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
-                        u8[i] = (b3 ? u16[i + 8] : u16[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u16[i] : u16[i + 8], 8);
+                        u8[i] = (b3 ? v[i + 8] : v[i]) + __shfl_xor_sync(0xffffffffu, b3 ? v[i] : v[i + 8], 8);
                     float u4[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
@@ -343,11 +326,11 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                     for (int i = 0; i < 2; ++i)
                         u2[i] = (b1 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b1 ? u4[i] : u4[i + 2], 2);
                     zsum = (b0 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b0 ? u2[0] : u2[1], 1);
-                    // + the tail of (row l >> 1, sample l & 1): this lane's half and the partner's
+                    // + the tail of (row trow, sample lane & 1): this lane's half and the partner's
                     const float other = __shfl_xor_sync(0xffffffffu, trs ? pt0 : pt1, 1);
                     zsum += (trs ? pt1 : pt0) + other;
                 }
-                if (trs == 0 || v1) sm.asum[(trs ? s1 : s0) % AR][kr0 + (lane >> 1)] = zsum;
+                if (trs == 0 || v1) sm.asum[(trs ? s1 : s0) % AR][trow] = zsum;
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sm.aready[s0 % AR]);
@@ -363,14 +346,14 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 mbar_wait_sleep(&sm.gready[ul % GR], (uint32_t)((ul / GR) & 1));
                 if (warp == 0) WS_TR(p, 6);
                 const int sl0 = u0 % S, sl1 = v1 ? u1 % S : S;
-                const float* xo0 = xring + sl0 * DP + 4 * lane;
-                const float* xo1 = xring + sl1 * DP + 4 * lane;
-                float gn0[RPW], gn1[RPW];               // -g of each row, samples u0, u1
+                const float* xo0 = xring + sl0 * DP + cl;
+                const float* xo1 = xring + sl1 * DP + cl;
+                float gn0[RW], gn1[RW];                 // -g of each of this lane's rows, samples u0, u1
                 {
-                    const float4* g0v = reinterpret_cast<const float4*>(&sm.gbuf[u0 % GR][kr0]);
-                    const float4* g1v = reinterpret_cast<const float4*>(&sm.gbuf[u1 % GR][kr0]);
+                    const float4* g0v = reinterpret_cast<const float4*>(&sm.gbuf[u0 % GR][kh]);
+                    const float4* g1v = reinterpret_cast<const float4*>(&sm.gbuf[u1 % GR][kh]);
 #pragma unroll
-                    for (int i = 0; i < RPW / 4; ++i) {
+                    for (int i = 0; i < RW / 4; ++i) {
                         const float4 a = g0v[i];
                         float4 b = g1v[i];
                         if (!v1) b = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -383,26 +366,19 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 #pragma unroll
                 for (int q = 0; q < (PNN_WS_EXP == 1 ? 0 : NQ); ++q) {
                     uint32_t tv[TQCOLS];
-                    tmem::ld32(tq + q * TQCOLS, tv);
-                    tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
+                    tmem::ld16(tq + q * TQCOLS, tv);
+                    tmem::ld4(tq + q * TQCOLS + 16, tv + 16);
                     uint64_t xa, xb, ya, yb;
-                    lds4(xo0 + 128 * q, xa, xb);
-                    lds4(xo1 + 128 * q, ya, yb);
+                    lds4(xo0 + 64 * q, xa, xb);
+                    lds4(xo1 + 64 * q, ya, yb);
 #pragma unroll
                     for (int r = 0; r < RR; ++r) {
                         w[r][2 * q] = ffma2(GP1(r), ya, ffma2(GP0(r), xa, w[r][2 * q]));
                         w[r][2 * q + 1] = ffma2(GP1(r), yb, ffma2(GP0(r), xb, w[r][2 * q + 1]));
                     }
-#pragma unroll
-                    for (int j = 0; j < NSR; ++j) {
-                        uint64_t* wp = reinterpret_cast<uint64_t*>(&sm.wsm[warp][j][q][lane]);
-                        const ulonglong2 ws = *reinterpret_cast<const ulonglong2*>(wp);
-                        wp[0] = ffma2(GP1(SR + j), ya, ffma2(GP0(SR + j), xa, ws.x));   // two 8-byte stores:
-                        wp[1] = ffma2(GP1(SR + j), yb, ffma2(GP0(SR + j), xb, ws.y));   // no re-pack MOVs
-                    }
                     tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
-                    for (int t = 0; t < TR; ++t) {
+                    for (int t = 0; t < TRW; ++t) {
                         const uint64_t a = ffma2(GP1(RR + t), ya, ffma2(GP0(RR + t), xa,
                                                  pk(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1]))));
                         const uint64_t b = ffma2(GP1(RR + t), yb, ffma2(GP0(RR + t), xb,
@@ -413,8 +389,8 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                         tv[4 * t] = __float_as_uint(a0); tv[4 * t + 1] = __float_as_uint(a1);
                         tv[4 * t + 2] = __float_as_uint(b0); tv[4 * t + 3] = __float_as_uint(b1);
                     }
-                    tmem::st32(tq + q * TQCOLS, tv);
-                    tmem::st8(tq + q * TQCOLS + 32, tv + 32);
+                    tmem::st16(tq + q * TQCOLS, tv);
+                    tmem::st4(tq + q * TQCOLS + 16, tv + 16);
                 }
                 {
                     uint32_t tt[8];
@@ -423,8 +399,8 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                     const float* xt1 = xring + sl1 * DP + XC + 8 * th8;
                     const float4 a0 = *reinterpret_cast<const float4*>(xt0), a1 = *reinterpret_cast<const float4*>(xt0 + 4);
                     const float4 c0 = *reinterpret_cast<const float4*>(xt1), c1 = *reinterpret_cast<const float4*>(xt1 + 4);
-                    const float ga = -sm.gbuf[u0 % GR][kr0 + trow];
-                    const float gb = v1 ? -sm.gbuf[u1 % GR][kr0 + trow] : 0.f;
+                    const float ga = -sm.gbuf[u0 % GR][trow];
+                    const float gb = v1 ? -sm.gbuf[u1 % GR][trow] : 0.f;
                     tmem::wait_ld_regs<8>(tt);
                     const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                     const float yv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -440,48 +416,40 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
             }
         }
 
-        // ---- write back this warp's W¹ rows (registers, TMEM, tail) ----
+        // ---- write back this lane's W¹ rows (registers, TMEM, tail) ----
 #pragma unroll
         for (int r = 0; r < RR; ++r) {
-            if (kr0 + r < H) {
-                float* dst = opaque(W1) + (long long)(kr0 + r) * D;
+            if (kh + r < H) {
+                float* dst = opaque(W1) + (long long)(kh + r) * D + cl;
 #pragma unroll
-                for (int m = 0; m < NP; ++m) *reinterpret_cast<uint64_t*>(dst + pcol(lane, m)) = w[r][m];
+                for (int q = 0; q < NQ; ++q) {
+                    *reinterpret_cast<uint64_t*>(dst + 64 * q) = w[r][2 * q];
+                    *reinterpret_cast<uint64_t*>(dst + 64 * q + 2) = w[r][2 * q + 1];
+                }
             }
         }
 #pragma unroll 1
         for (int q = 0; q < NQ; ++q) {
             uint32_t tv[TQCOLS];
-            tmem::ld32(tq + q * TQCOLS, tv);
-            tmem::ld8(tq + q * TQCOLS + 32, tv + 32);
+            tmem::ld16(tq + q * TQCOLS, tv);
+            tmem::ld4(tq + q * TQCOLS + 16, tv + 16);
             tmem::wait_ld_regs<TQCOLS>(tv);
 #pragma unroll
-            for (int t = 0; t < TR; ++t) {
-                if (kr0 + RR + t < H) {
-                    float* dst = opaque(W1) + (long long)(kr0 + RR + t) * D + 4 * lane + 128 * q;
+            for (int t = 0; t < TRW; ++t) {
+                if (kh + RR + t < H) {
+                    float* dst = opaque(W1) + (long long)(kh + RR + t) * D + cl + 64 * q;
                     *reinterpret_cast<float2*>(dst) = make_float2(__uint_as_float(tv[4 * t]), __uint_as_float(tv[4 * t + 1]));
                     *reinterpret_cast<float2*>(dst + 2) =
                         make_float2(__uint_as_float(tv[4 * t + 2]), __uint_as_float(tv[4 * t + 3]));
                 }
             }
         }
-#pragma unroll
-        for (int j = 0; j < NSR; ++j) {
-            if (kr0 + SR + j >= H) continue;
-            float* dst = opaque(W1) + (long long)(kr0 + SR + j) * D + 4 * lane;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const float4 v4 = sm.wsm[warp][j][q][lane];
-                *reinterpret_cast<float2*>(dst + 128 * q) = make_float2(v4.x, v4.y);
-                *reinterpret_cast<float2*>(dst + 128 * q + 2) = make_float2(v4.z, v4.w);
-            }
-        }
         {
             uint32_t tt[8];
             tmem::ld8(tq + TTAIL, tt);
             tmem::wait_ld_regs<8>(tt);
-            if (kr0 + trow < H) {
-                float* dst = opaque(W1) + (long long)(kr0 + trow) * D + XC + 8 * th8;
+            if (trow < H) {
+                float* dst = opaque(W1) + (long long)trow * D + XC + 8 * th8;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (XC + 8 * th8 + j < D) dst[j] = __uint_as_float(tt[j]);
@@ -556,7 +524,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 const float* xc = xring + ((s1 - 5 >= 0) ? (s1 - 5) % S : S) * DP;
                 uint64_t ga = 0ull, gc = 0ull;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
+                for (int q = 0; q < NQG; ++q) {
                     uint64_t a0, a1, b0, b1v;
                     lds4(xa + 4 * lane + 128 * q, a0, a1);
                     lds4(xb + 4 * lane + 128 * q, b0, b1v);
@@ -566,7 +534,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 // k = 5: warp cw takes quads cw and cw + 4 (warps 2, 3: quad cw only; warp 3 the tail)
                 uint64_t gc2 = 0ull;
                 {
-                    const int qb = (cw + 4 < NQ) ? cw + 4 : cw;
+                    const int qb = (cw + 4 < NQG) ? cw + 4 : cw;
                     uint64_t a0, a1, c0, c1;
                     lds4(xa + 4 * lane + 128 * cw, a0, a1);
                     lds4(xc + 4 * lane + 128 * cw, c0, c1);
@@ -581,7 +549,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 upk(gc, lo, hi);
                 float gw = lo + hi;
                 upk(gc2, lo, hi);
-                gw += (cw + 4 < NQ) ? lo + hi : 0.f;
+                gw += (cw + 4 < NQG) ? lo + hi : 0.f;
                 {                                       // columns 768 + 4·(lane & 3) .. +3 (zero past D)
                     const float4 a = *reinterpret_cast<const float4*>(xa + XC + 4 * (lane & 3));
                     const float4 b = *reinterpret_cast<const float4*>(xb + XC + 4 * (lane & 3));
