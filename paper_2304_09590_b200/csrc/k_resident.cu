@@ -194,123 +194,6 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
     }
 }
 
-// The same records, with the rows streamed through a per-warp ring of GNB shared-memory slots by
-// 1-D bulk copies (GNB rows in flight per warp instead of one register prefetch): each lane loads
-// its 28 columns of a row from shared memory, so the arithmetic (and the records, bit for bit) is
-// gram_kernel's.  Needs D % 4 == 0 (16-byte bulk copies); launch_gram falls back otherwise.
-constexpr int GNB = 4;          // ring slots per warp
-constexpr int GWP = 4;          // warps per CTA
-constexpr int GCH2 = 64;        // rows per chunk
-constexpr int GDP = 800;        // slot stride (floats)
-__global__ void __launch_bounds__(GWP * 32)
-gram_ring_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, long long n_local,
-                 int K_local, int s_first, int s_count, float4* __restrict__ rec) {
-    extern __shared__ __align__(128) unsigned char gsm[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gsm);                       // [GWP][GNB]
-    float* ring = reinterpret_cast<float*>(gsm + 128);                        // [GWP][GNB][GDP]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* wb = bars + warp * GNB;
-    float* wr = ring + (size_t)warp * GNB * GDP;
-    if (lane == 0)
-        for (int i = 0; i < GNB; ++i) mbar_init(&wb[i], 1);
-    fence_mbar_init();
-    __syncwarp();
-    long long r0, c0, r1, c1;
-    shard_of(n_local, K_local, s_first, &r0, &c0);
-    shard_of(n_local, K_local, s_first + s_count - 1, &r1, &c1);
-    const long long rows = r1 + c1 - r0;
-    const long long base = n_local / K_local, rem = n_local % K_local;
-    auto shard_start = [&](long long row) {       // first row of the CN owning `row` (R17)
-        const long long sidx = (row < rem * (base + 1)) ? row / (base + 1)
-                                                        : rem + (row - rem * (base + 1)) / base;
-        long long st, cnt;
-        shard_of(n_local, K_local, (int)sidx, &st, &cnt);
-        return st;
-    };
-    const uint32_t rbytes = (uint32_t)D * 4u;
-    auto issue = [&](long long row, int slot) {
-        mbar_arrive_expect_tx(&wb[slot], rbytes);
-        bulk_g2s(wr + slot * GDP, X + row * (long long)D, rbytes, &wb[slot]);
-    };
-    auto dot = [](const float4 (&a)[7], const float4 (&b)[7]) {
-        float s = 0.f;
-#pragma unroll
-        for (int q = 0; q < 7; ++q)
-            s = fmaf(a[q].w, b[q].w, fmaf(a[q].z, b[q].z, fmaf(a[q].y, b[q].y, fmaf(a[q].x, b[q].x, s))));
-        return s;
-    };
-    const bool tl = 4 * lane + 768 < D;
-    long long g = 0;                               // rows this warp has streamed (ring phase)
-    const long long nwarps = (long long)gridDim.x * GWP;
-    const long long nchunks = (rows + GCH2 - 1) / GCH2;
-    for (long long ch = blockIdx.x * (long long)GWP + warp; ch < nchunks; ch += nwarps) {
-        const long long a0 = r0 + ch * GCH2, a1 = min(a0 + GCH2, r0 + rows);
-        const long long st = shard_start(a0);
-        const long long p0 = max(a0 - 5, st);      // stream rows p0 .. a1-1 (earlier ones are zero)
-        const int n = (int)(a1 - p0);
-        if (lane == 0)
-            for (int i = 0; i < GNB && i < n; ++i) issue(p0 + i, (int)((g + i) % GNB));
-        float4 win[5][7];                          // win[k] = x(row - 5 + k)
-#pragma unroll
-        for (int k = 0; k < 5; ++k)
-#pragma unroll
-            for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int i = 0; i < n; ++i, ++g) {
-            const long long row = p0 + i;
-            const int slot = (int)(g % GNB);
-            mbar_wait(&wb[slot], (uint32_t)((g / GNB) & 1));
-            const float* xs = wr + slot * GDP;
-            float4 cur[7];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) cur[q] = *reinterpret_cast<const float4*>(xs + 4 * lane + 128 * q);
-            cur[6] = tl ? *reinterpret_cast<const float4*>(xs + 768 + 4 * lane) : make_float4(0.f, 0.f, 0.f, 0.f);
-            __syncwarp();                          // every lane has read the slot
-            if (lane == 0 && i + GNB < n) issue(row + GNB, slot);
-            if (row > p0 && shard_start(row) == row) {   // a new slice begins: no terms before it
-#pragma unroll
-                for (int k = 0; k < 5; ++k)
-#pragma unroll
-                    for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            if (row >= a0) {
-                float gk[5];
-#pragma unroll
-                for (int k = 0; k < 5; ++k) gk[k] = warp_sum(dot(win[k], cur));
-                if (lane == 0) {                   // {G(u-4..u-1)}, {label, G(u-5)}
-                    rec[2 * row] = make_float4(gk[1], gk[2], gk[3], gk[4]);
-                    rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), gk[0], 0.f, 0.f);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int q = 0; q < 7; ++q) win[k][q] = win[k + 1][q];
-#pragma unroll
-            for (int q = 0; q < 7; ++q) win[4][q] = cur[q];
-        }
-    }
-}
-
-static cudaError_t launch_gram_any(const float* x, const int32_t* labels, int D, long long n_local, int K_local,
-                                   int s_first, int s_count, float4* rec, cudaStream_t st) {
-    if (s_count <= 0) return cudaSuccess;
-    if (D % 4 != 0 || D > GDP) {
-        gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, D, n_local, K_local, s_first, s_count, rec);
-        return cudaGetLastError();
-    }
-    const size_t smem = 128 + sizeof(float) * (size_t)GWP * GNB * GDP;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaError_t e = cudaFuncSetAttribute(gram_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    gram_ring_kernel<<<2 * nsm, GWP * 32, smem, st>>>(x, labels, D, n_local, K_local, s_first, s_count, rec);
-    return cudaGetLastError();
-}
-
 template <int C, int A1, int A2, bool TRACE>
 __global__ void __launch_bounds__(NW * 32, 1)
 sgd_resident_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ X,
@@ -1226,7 +1109,9 @@ cudaError_t launch_c(const ResidentPlan& p, const NetDesc& d, float* children, c
 // The Gram-record pre-pass, for other kernels that use the same lookahead (k_deep.cu).
 cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
                         int s_count, float4* rec, cudaStream_t st) {
-    return launch_gram_any(x, labels, D, n_local, K_local, s_first, s_count, rec, st);
+    if (s_count <= 0) return cudaSuccess;
+    gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, D, n_local, K_local, s_first, s_count, rec);
+    return cudaGetLastError();
 }
 
 ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int variant) {
@@ -1316,7 +1201,8 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
         if (e != cudaSuccess || !ev1) return e;
         return cudaEventRecord(ev1, st);
     }
-    e = launch_gram_any(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec, st);
+    gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (ev0) {                                     // timing hook: bracket the SGD launch only
         if ((e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
