@@ -153,8 +153,16 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
     const long long nchunks = (rows + GCH - 1) / GCH;
     for (long long ch = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
         const long long a0 = r0 + ch * GCH, a1 = min(a0 + GCH, r0 + rows);
-        float4 win[5][7];                          // win[k] = x(row - 5 + k), k = 0..4
+        float4 win[5][7];                          // win[k] = x(row - 5 + k)
         const long long st = shard_start(a0);
+        // the next slice boundary after a0 (no per-row division: the rows are walked in order)
+        long long nxt_start;
+        {
+            const long long sidx = (a0 < rem * (base + 1)) ? a0 / (base + 1) : rem + (a0 - rem * (base + 1)) / base;
+            long long s1, c1;
+            shard_of(n_local, K_local, (int)sidx, &s1, &c1);
+            nxt_start = s1 + c1;
+        }
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
             const long long pr = a0 - 5 + k;
@@ -166,12 +174,12 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
         float4 nxt[7];
         load(a0, nxt);
         for (long long row = a0; row < a1; ++row) {
-            const long long s0 = shard_start(row);
-            if (s0 == row && row != a0) {          // a new slice begins: no terms before it
+            if (row == nxt_start) {                // a new slice begins: no terms before it
 #pragma unroll
                 for (int k = 0; k < 5; ++k)
 #pragma unroll
                     for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                nxt_start += base + ((row < rem * (base + 1)) ? 1 : 0);   // R17: slices before rem are base+1 long
             }
             float4 cur[7];
 #pragma unroll
