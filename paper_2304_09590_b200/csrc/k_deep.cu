@@ -653,8 +653,16 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
                 for (int m = 0; m < RW2; ++m) a2[m] += __shfl_xor_sync(0xffffffffu, a2[m], o);
             DTR(11);
             float h2v[RW2];
+            {                                       // branch-free: the RW2 activations interleave
+                float bz[RW2];
 #pragma unroll
-            for (int m = 0; m < RW2; ++m) h2v[m] = rv[m] ? act_fast<A2>(a2[m] + sm.b2s[cw + NCW * m]) : 0.f;
+                for (int m = 0; m < RW2; ++m) bz[m] = sm.b2s[cw + NCW * m];   // (rows past own2: unused)
+#pragma unroll
+                for (int m = 0; m < RW2; ++m) {
+                    const float t = act_fast<A2>(a2[m] + bz[m]);
+                    h2v[m] = rv[m] ? t : 0.f;
+                }
+            }
             DTR(12);
             // ---- this warp's partial logits W³[:, rows]·h2 → every CTA ----
             {
@@ -708,16 +716,17 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
             }
             // ---- δ2 of this warp's rows (pre-update W³, R6); W³, b2 updates ----
             float d2[RW2];
+            {                                       // branch-free loads, predicated stores
+                const int ol = lane < O ? lane : 0;
+                float w3v[RW2];
 #pragma unroll
-            for (int m = 0; m < RW2; ++m) {
-                const int i = cw + NCW * m;
-                float t = 0.f;
-                if (lane < O) {
-                    const float w3 = sm.w3s[lane][i];
-                    t = w3 * d3;
-                    sm.w3s[lane][i] = fmaf(-lr * d3, h2v[m], w3);   // invalid rows: h2 = 0
+                for (int m = 0; m < RW2; ++m) w3v[m] = sm.w3s[ol][cw + NCW * m];
+                const float e3 = -lr * d3;          // d3 = 0 for lanes >= O
+#pragma unroll
+                for (int m = 0; m < RW2; ++m) {
+                    d2[m] = w3v[m] * d3;
+                    if (lane < O) sm.w3s[lane][cw + NCW * m] = fmaf(e3, h2v[m], w3v[m]);   // invalid rows: h2 = 0
                 }
-                d2[m] = t;
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
