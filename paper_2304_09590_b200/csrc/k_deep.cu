@@ -732,10 +732,14 @@ sgd_deep_kernel(NetDesc d, float* __restrict__ children, const float* __restrict
             for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
                 for (int m = 0; m < RW2; ++m) d2[m] += __shfl_xor_sync(0xffffffffu, d2[m], o);
+            {                                       // lane m < RW2 updates b2 of row m (one store per lane)
+                float dsel = 0.f;
 #pragma unroll
-            for (int m = 0; m < RW2; ++m) {
-                d2[m] = rv[m] ? d2[m] * act_deriv_t<A2>(h2v[m]) : 0.f;
-                if (lane == 0 && rv[m]) sm.b2s[cw + NCW * m] -= lr * d2[m];
+                for (int m = 0; m < RW2; ++m) {
+                    d2[m] = rv[m] ? d2[m] * act_deriv_t<A2>(h2v[m]) : 0.f;
+                    dsel = (lane == m) ? d2[m] : dsel;
+                }
+                if (lane < RW2 && cw + NCW * lane < own2) sm.b2s[cw + NCW * lane] -= lr * dsel;
             }
             DTR(6);
             // ---- fused: partial (W²ᵀδ2)_j over this warp's rows (pre-update, R6) → unit j's
