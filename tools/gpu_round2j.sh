@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-2 final batch (j): full GPU tests (incl. slow), smoke, bench lines for every config, the reference
+# arm, C4 variants, C4 + C3 launch lists, ncu full captures of the v12 SGD launch and the deep kernel,
+# clock64 traces of both.
+cd "$(dirname "$0")/.." || exit 1
+O=gpurun_out/r2j; mkdir -p $O
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
+timeout 900 python bench.py > $O/bench_C4.json 2> $O/bench_C4.err; echo "bench C4 rc=$?"
+timeout 300 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref_C4.json 2>&1; echo "ref rc=$?"
+for c in C1 C2 C3 C5 F1; do timeout 900 python bench.py --config $c --steps 3 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err; echo "bench $c rc=$?"; done
+for v in v8 tmem; do timeout 600 python bench.py --variant $v --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C4_$v.json 2>&1; echo "bench C4 $v rc=$?"; done
+B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 300 $B > $O/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C4.csv $B > /dev/null 2>&1; echo "launches C4 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgd_ws -s 3 -c 1 -o $O/prof_ws_C4 $B > $O/ncu.log 2>&1; echo "ncu C4 rc=$?"
+B3="python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 300 $B3 > $O/plain3.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C3.csv $B3 > /dev/null 2>&1; echo "launches C3 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgd_deep -s 3 -c 1 -o $O/prof_deep_C3 $B3 > $O/ncu3.log 2>&1; echo "ncu C3 rc=$?"
+PNN_LIB=$PWD/paper_2304_09590_b200/libpnn_tr.so timeout 300 python tools/trace_ws.py > $O/trace_ws.txt 2>&1; echo "trace ws rc=$?"
+timeout 300 python tools/trace_deep.py --config C3 --K 32 --rows 1875 > $O/trace_deep.txt 2>&1; echo "trace deep rc=$?"
