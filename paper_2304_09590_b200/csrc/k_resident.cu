@@ -1202,10 +1202,9 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
                                 cudaEvent_t ev0, cudaEvent_t ev1) {
     if (s_count <= 0) return cudaSuccess;
     cudaError_t e;
-    if (p.variant == 11 || (p.variant == 12 && !kWsPrepass)) {   // v11 forms its Gram terms in the launch
+    if (p.variant == 11) {                         // v11 forms its Gram terms in the launch
         if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
-        e = p.variant == 11 ? launch_sgd_tmem(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st)
-                            : launch_sgd_ws(d, children, x, labels, nullptr, n_local, K_local, s_first, s_count, lr, st);
+        e = launch_sgd_tmem(d, children, x, labels, n_local, K_local, s_first, s_count, lr, st);
         if (e != cudaSuccess || !ev1) return e;
         return cudaEventRecord(ev1, st);
     }

@@ -8,24 +8,26 @@
 // Eqs.2-13): z1 = W1 x + b1, h = φ1(z1); z2 = W2 h + b2; δ2 (Eq.10 softmax+CE, or Eq.9 / R11);
 // δ1 = (W2ᵀδ2) ⊙ φ1'(h) with the pre-update W2 (R6); W -= η δ xᵀ, b -= η δ (Eqs.12-13).
 //
-// Same data layout and L = 4 lookahead as v11 (k_tmem.cu, R27):
+// The R27 lookahead: with W¹(t) the weights before sample t's update and
+// g(s) = η δ1(s),
 //     z1(t) = W¹(t-L) x(t) - Σ_{k=1..L} g(t-k)·G(t-k,t) + b1(t),  G(s,t) = x(s)·x(t),
-// with W¹'s 128 rows split between the register file (6 rows per sweep warp) and tensor
-// memory (10 rows per sweep warp + the 16-column tail).  What differs is who runs the chain.
-// In v11 the chain of sample c runs on a rotating pair of the 8 sweep warps, whose sweeps
-// stop for the chain's whole latency: measured, the per-sample period (~4,300 cycles) was the
-// sweep time plus most of a chain.  Here 12 warps in three warpgroups:
-//   warps 0-7  (setmaxnreg ↑ kSweepRegs): sweeps only — F(s) = W¹(s-L)·x(s) (row sums to
-//              shared memory, arrive aready(s)), U(s) = W¹ -= g(s-L)·x(s-L)ᵀ (wait gready(s-L));
+// the paper's pre-activation in real arithmetic; L = 4 for even and 5 for odd samples (paired
+// sweeps).  The Gram terms and labels come from gram_kernel's 32-B records.  W¹'s 128 rows sit
+// in the register file and tensor memory of ONE SM, as in v11 (k_tmem.cu); what differs is who
+// runs the per-sample chain.  In v11 it runs on a rotating pair of the 8 sweep warps, whose
+// sweeps stop for the chain's whole latency (period ~4,300 cycles per sample: sweep time plus
+// most of a chain).  Here 12 warps in three warpgroups:
+//   warps 0-7  (setmaxnreg ↑ kSweepRegs): sweeps only — paired F(2p), F(2p+1) = W¹(2p-4)·x
+//              (row sums to shared memory, arrive aready), then U(2p-4), U(2p-3)
+//              (W¹ -= g·xᵀ in sample order, after gready);
 //   warps 8-11 (setmaxnreg ↓ kChainRegs): the chain of every sample, one hidden unit per
-//              thread (u = 32·(warp-8) + lane) with W2[:, u], b1[u] and g(c-1..c-4)[u] in
+//              thread (u = 32·(warp-8) + lane) with W2[:, u], b1[u] and g(c-1..c-5)[u] in
 //              registers; the four warps' partial logits meet through shared memory and a named
-//              barrier; g(c) goes to shared memory (arrive gready(c)).  The chain warps also
-//              form the Gram terms G(c+1-k, c+1) (warp k-1) one sample ahead, stage the labels
-//              and issue the x bulk copies.
+//              barrier; lane o < 10 forms z2_o and δ2_o (softmax by shuffles); g(c) goes to shared
+//              memory (arrive gready(c)); the chain warps also issue the x bulk copies.
 // The sweeps never run chain code and the chain never waits for a sweep except through
-// aready(c) (whose F(c) ran L samples ahead of the chain's need), so the period is
-// max(sweep, chain) instead of their sum.
+// aready(c) (F(c) ran L samples ahead of the chain's need), so the period is max(sweep, chain)
+// instead of their sum (C4 0.542 of FP32 FMA peak for this launch).
 #include <cstddef>
 #include <cstdio>
 #include "pnn_internal.h"
@@ -33,9 +35,6 @@
 #include "pnn_ptx.cuh"
 #include "pnn_tmem.cuh"
 
-#ifndef PNN_WS_EXP
-#define PNN_WS_EXP 0   // experiment builds only: 1 = sweeps without FMAs, 2 = chain without compute
-#endif
 #ifdef PNN_WS_TRACE
 // experiment builds only: clock64 timeline of CTA 0 (tools/trace_ws.py): [i < 256][point < 8]
 #define WS_TR(i, pt) do { if (trace && blockIdx.x == 0 && lane == 0 && (i) < 256) trace[(i) * 8 + (pt)] = ptx::clock64(); } while (0)
@@ -57,10 +56,9 @@ constexpr int TRW = RW - RR;    // and in TMEM
 constexpr int UMAX = NSW * RPW; // 128 hidden units
 constexpr int NQ = 12;          // column quads per lane (4 columns each, stride 64): columns [0, 768)
 constexpr int NP = 2 * NQ;      // f32x2 pairs per lane per row
-constexpr int NQG = 6;          // the chain's Gram dot products: quads of 32 lanes x 4 columns (stride 128)
 constexpr int XC = 768;         // first tail column
 constexpr int DP = 800;         // x ring slot stride (floats)
-constexpr int GOFF = 784;       // PRE: the Gram record of x(u) at its slot + GOFF
+constexpr int GOFF = 784;       // the Gram record of x(u) at its ring slot + GOFF
 constexpr int LAG = 4;          // lookahead L
 constexpr int S = 16;           // x ring slots (+ one zero row at slot S)
 constexpr int PF = 8;           // prefetch distance: x(c+PF) issued after chain c
@@ -91,7 +89,6 @@ struct __align__(16) Smem {
     float asum[AR][UMAX];       // [s % AR][unit] row sums W¹(s-L)·x(s)
     float gbuf[GR][UMAX];       // [c % GR][unit] g(c) = η δ1(c)
     float zp[2][NCW][16];       // [c & 1][chain warp][o] partial logits
-    float gpart[GT][8];         // [s % GT][j] j < 4: G(s-1-j, s); 4 + w: chain warp w's quarter of G(s-5, s)
     float b2s[2][12];           // b2 before sample c at [c & 1]
 };
 constexpr size_t kSmemHead = ((sizeof(Smem) + 127) / 128) * 128;
@@ -141,9 +138,10 @@ __device__ __forceinline__ float treduce16(const float (&v)[16], int lane) {
     return (b1 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? u2[0] : u2[1], 2);
 }
 
-// PRE: the Gram terms and the label come with x(u) through the ring as the 32-B record of
-// gram_kernel (k_resident.cu; launch_gram) instead of being formed by the chain warps.
-template <int A1, int A2, bool PRE>
+// The Gram terms and the label come with x(u) through the ring as the 32-B record of gram_kernel
+// (k_resident.cu, launch_gram).  (Forming them in the chain warps instead, one sample ahead, made
+// the chain the limit: 12.39 ms per C4 epoch against 10.63 + 0.86 ms.)
+template <int A1, int A2>
 __global__ void __launch_bounds__(NT, 1)
 sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__ X, const int32_t* __restrict__ Y,
               const float4* __restrict__ rec, long long n_local, int K_local, int s_first, float lr,
@@ -164,7 +162,6 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
     float* W2 = b1g + H;
     float* b2g = W2 + (long long)O * H;
     const float* Xc = X + row0 * (long long)D;
-    const int32_t* Yc = Y + row0;
     const uint32_t xbytes = (uint32_t)D * 4u;
 
     if (warp == 0) tmem::alloc(&sm.tbase, 512);
@@ -253,7 +250,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 #pragma unroll
                 for (int r = 0; r < RW; ++r) { acc0[r] = 0ull; acc1[r] = 0ull; }
 #pragma unroll
-                for (int q = 0; q < (PNN_WS_EXP == 1 ? 0 : NQ); ++q) {
+                for (int q = 0; q < NQ; ++q) {
                     uint32_t tv[TQCOLS];
                     tmem::ld16(tq + q * TQCOLS, tv);
                     tmem::ld4(tq + q * TQCOLS + 16, tv + 16);
@@ -364,7 +361,7 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 #define GP0(r) pk(gn0[r], gn0[r])
 #define GP1(r) pk(gn1[r], gn1[r])
 #pragma unroll
-                for (int q = 0; q < (PNN_WS_EXP == 1 ? 0 : NQ); ++q) {
+                for (int q = 0; q < NQ; ++q) {
                     uint32_t tv[TQCOLS];
                     tmem::ld16(tq + q * TQCOLS, tv);
                     tmem::ld4(tq + q * TQCOLS + 16, tv + 16);
@@ -470,40 +467,25 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
         const float4* Rc = rec + 2 * row0;
         auto issue_x = [&](int s) {
             uint64_t* bar = &sm.xfull[s % S];
-            mbar_arrive_expect_tx(bar, xbytes + (PRE ? 32u : 0u));
+            mbar_arrive_expect_tx(bar, xbytes + 32u);
             bulk_g2s(xring + (s % S) * DP, Xc + (long long)s * D, xbytes, bar);
-            if constexpr (PRE) bulk_g2s(xring + (s % S) * DP + GOFF, Rc + 2 * s, 32u, bar);
+            bulk_g2s(xring + (s % S) * DP + GOFF, Rc + 2 * s, 32u, bar);
         };
         if (leader)
             for (int s = 0; s < PF && s < T; ++s) issue_x(s);
-        int lab0 = (T > 0) ? __ldg(Yc) : 0;          // labels of samples c, c+1
-        int lab1 = (T > 1) ? __ldg(Yc + 1) : 0;
         for (int c = 0; c < T; ++c) {
-            const int lab2 = (!PRE && c + 2 < T) ? __ldg(Yc + c + 2) : 0;
             // ---- z1(c) = acc - Σ_k g(c-k) G(c-k,c) + b1(c), h(c) ----
             if (cw == 0) WS_TR(c, 0);
-            if constexpr (PRE) mbar_wait_sleep(&sm.xfull[c % S], (uint32_t)((c / S) & 1));   // x(c)'s record
-            else if (c + 1 < T) mbar_wait_sleep(&sm.xfull[(c + 1) % S], (uint32_t)(((c + 1) / S) & 1));   // for G(·, c+1)
+            mbar_wait_sleep(&sm.xfull[c % S], (uint32_t)((c / S) & 1));   // x(c)'s record
             mbar_wait_sleep(&sm.aready[c % AR], (uint32_t)((c / AR) & 1));
             if (cw == 0) WS_TR(c, 1);
-            if constexpr (PNN_WS_EXP == 2) {
-                sm.gbuf[c % GR][u] = 0.f;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.gready[c % GR]);
-                if (leader && c + PF < T) issue_x(c + PF);
-                continue;
-            }
-            float G[5];                             // G(c-k, c), k = 1..5 (formed during chain c-1)
-            if constexpr (PRE) {                    // {G(c-4), G(c-3), G(c-2), G(c-1)}, {label, G(c-5)}
+            float G[5];                             // G(c-k, c), k = 1..5
+            int lab0;
+            {                                       // {G(c-4), G(c-3), G(c-2), G(c-1)}, {label, G(c-5)}
                 const float4 r0 = *reinterpret_cast<const float4*>(xring + (c % S) * DP + GOFF);
                 const float2 r1 = *reinterpret_cast<const float2*>(xring + (c % S) * DP + GOFF + 4);
                 G[0] = r0.w; G[1] = r0.z; G[2] = r0.y; G[3] = r0.x; G[4] = r1.y;
                 lab0 = __float_as_int(r1.x);
-            } else {
-                const float4 g4v = *reinterpret_cast<const float4*>(&sm.gpart[c % GT][0]);
-                const float4 g5v = *reinterpret_cast<const float4*>(&sm.gpart[c % GT][4]);
-                G[0] = g4v.x; G[1] = g4v.y; G[2] = g4v.z; G[3] = g4v.w;
-                G[4] = (g5v.x + g5v.y) + (g5v.z + g5v.w);
             }
             float z = sm.asum[c % AR][u];
             if (c & 1) z = fmaf(-g5, G[4], z);
@@ -513,62 +495,6 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
             z = fmaf(-g1, G[0], z);
             z += b1;
             const float h = lc ? act_fwd_t<A1>(z) : 0.f;
-            if constexpr (!PRE)
-            // ---- G(c+1-k, c+1): term k = cw + 1 over all columns, and a quarter of the k = 5 term
-            //      (odd samples; the paired sweeps' odd samples miss 5 updates), branch-free so the
-            //      compiler interleaves it with the partial logits below (R27) ----
-            {
-                const int s1 = c + 1;                   // (s1 = T: any slot; nothing is stored)
-                const float* xa = xring + (s1 % S) * DP;
-                const float* xb = xring + ((s1 - 1 - cw >= 0) ? (s1 - 1 - cw) % S : S) * DP;
-                const float* xc = xring + ((s1 - 5 >= 0) ? (s1 - 5) % S : S) * DP;
-                uint64_t ga = 0ull, gc = 0ull;
-#pragma unroll
-                for (int q = 0; q < NQG; ++q) {
-                    uint64_t a0, a1, b0, b1v;
-                    lds4(xa + 4 * lane + 128 * q, a0, a1);
-                    lds4(xb + 4 * lane + 128 * q, b0, b1v);
-                    ga = ffma2(a0, b0, ga);
-                    ga = ffma2(a1, b1v, ga);
-                }
-                // k = 5: warp cw takes quads cw and cw + 4 (warps 2, 3: quad cw only; warp 3 the tail)
-                uint64_t gc2 = 0ull;
-                {
-                    const int qb = (cw + 4 < NQG) ? cw + 4 : cw;
-                    uint64_t a0, a1, c0, c1;
-                    lds4(xa + 4 * lane + 128 * cw, a0, a1);
-                    lds4(xc + 4 * lane + 128 * cw, c0, c1);
-                    gc = ffma2(a1, c1, ffma2(a0, c0, gc));
-                    lds4(xa + 4 * lane + 128 * qb, a0, a1);
-                    lds4(xc + 4 * lane + 128 * qb, c0, c1);
-                    gc2 = ffma2(a1, c1, ffma2(a0, c0, gc2));
-                }
-                float lo, hi;
-                upk(ga, lo, hi);
-                float gv = lo + hi;
-                upk(gc, lo, hi);
-                float gw = lo + hi;
-                upk(gc2, lo, hi);
-                gw += (cw + 4 < NQG) ? lo + hi : 0.f;
-                {                                       // columns 768 + 4·(lane & 3) .. +3 (zero past D)
-                    const float4 a = *reinterpret_cast<const float4*>(xa + XC + 4 * (lane & 3));
-                    const float4 b = *reinterpret_cast<const float4*>(xb + XC + 4 * (lane & 3));
-                    const float4 e = *reinterpret_cast<const float4*>(xc + XC + 4 * (lane & 3));
-                    const float tb = fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
-                    const float te = fmaf(a.w, e.w, fmaf(a.z, e.z, fmaf(a.y, e.y, a.x * e.x)));
-                    gv += (lane < 4) ? tb : 0.f;
-                    gw += (lane < 4 && cw == 3) ? te : 0.f;
-                }
-                // lanes < 16 end with Σ gv, lanes >= 16 with Σ gw
-                const bool hi16 = lane & 16;
-                float gg = (hi16 ? gw : gv) + __shfl_xor_sync(0xffffffffu, hi16 ? gv : gw, 16);
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) gg += __shfl_xor_sync(0xffffffffu, gg, o);
-                if (s1 < T) {
-                    if (lane == 0) sm.gpart[s1 % GT][cw] = gg;
-                    if (lane == 16) sm.gpart[s1 % GT][4 + cw] = gg;
-                }
-            }
             // ---- this warp's partial logits Σ_u W2[o][u] h_u ----
             {
                 float pv[16];
@@ -628,8 +554,6 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 // Gram read of x(c-3): the slot of x(c+PF-S) is free
                 if (c + PF < T) issue_x(c + PF);
             }
-            lab0 = lab1;
-            lab1 = lab2;
         }
         if (lc) {
 #pragma unroll
@@ -650,7 +574,8 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
 template <int A1, int A2>
 cudaError_t launch_one(const NetDesc& d, float* children, const float* x, const int32_t* y, const float4* rec,
                        long long n_local, int K_local, int s_first, int s_count, float lr, cudaStream_t st) {
-    auto kern = rec ? sgd_ws_kernel<A1, A2, true> : sgd_ws_kernel<A1, A2, false>;
+    if (!rec) return cudaErrorInvalidValue;        // the Gram records of launch_gram are required
+    auto kern = sgd_ws_kernel<A1, A2>;
     const size_t smem = kSmemHead + sizeof(float) * (size_t)(S + 1) * DP;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

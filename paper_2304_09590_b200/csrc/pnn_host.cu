@@ -245,8 +245,7 @@ pnn_status launch_train_wave(pnn_net net, const float* x, const int32_t* y, long
         if (k != PNN_KERNEL_RESIDENT) CUDA_TRY(net, cudaEventRecord(ev0, st));   // the resident path
     }                                                                               // brackets its SGD launch
     const bool deep = var == PNN_VARIANT_CLUSTER_DEEP;
-    const bool gram = deep || (k == PNN_KERNEL_RESIDENT && var != PNN_VARIANT_RESIDENT_TMEM &&
-                               (var != PNN_VARIANT_RESIDENT_WS || kWsPrepass));
+    const bool gram = deep || (k == PNN_KERNEL_RESIDENT && var != PNN_VARIANT_RESIDENT_TMEM);
     if (gram && net->gram_rows < n) {                                // 32-B Gram records (R27)
         cudaFree(net->d_gram);
         net->d_gram = nullptr;
@@ -780,8 +779,7 @@ pnn_status pnn_kernel_info(pnn_net net, int32_t* kernel, int32_t* launches) {
     // forms its Gram terms in the training launch; tc bf16: 7 per mini-batch step; fp32 step
     // kernels: 4 per step; MB_RESIDENT: 1 per epoch
     const bool gram = v == PNN_VARIANT_CLUSTER_DEEP ||
-                      (k == PNN_KERNEL_RESIDENT && v != PNN_VARIANT_RESIDENT_TMEM &&
-                       (v != PNN_VARIANT_RESIDENT_WS || kWsPrepass));
+                      (k == PNN_KERNEL_RESIDENT && v != PNN_VARIANT_RESIDENT_TMEM);
     *launches = gram ? 2 : (k == PNN_KERNEL_TC_BF16) ? 7 : (k == PNN_KERNEL_MB_F32) ? 4 : 1;
     return PNN_OK;
 }

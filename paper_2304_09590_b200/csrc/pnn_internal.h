@@ -67,17 +67,11 @@ cudaError_t launch_sgd_tmem(const NetDesc& d, float* children, const float* x, c
                             int K_local, int s_first, int s_count, float lr, cudaStream_t st);
 
 // Warp-specialised TMEM variant (k_ws.cu, v12): as v11 with the per-sample chain on its own
-// warpgroup.  nullptr when the shape is supported.
+// warpgroup.  nullptr when the shape is supported.  rec: the Gram records of launch_gram (the
+// chain reads the terms and the labels from the x ring).
 const char* ws_plan(const NetDesc& d, int batch);
-// rec: the Gram records of launch_gram (the chain reads the terms and labels from the x ring),
-// or nullptr: the chain warps form the terms in the launch and read labels from y.
 cudaError_t launch_sgd_ws(const NetDesc& d, float* children, const float* x, const int32_t* y, const float4* rec,
                           long long n_local, int K_local, int s_first, int s_count, float lr, cudaStream_t st);
-#ifndef PNN_WS_INLAUNCH_GRAM
-constexpr bool kWsPrepass = true;    // v12 takes the Gram pre-pass (measured faster)
-#else
-constexpr bool kWsPrepass = false;
-#endif
 
 // The lookahead's Gram records (32 B per row: x(u-4..u-1)·x(u) and the label), k_resident.cu.
 cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
