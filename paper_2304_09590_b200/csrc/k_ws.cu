@@ -242,8 +242,8 @@ sgd_ws_kernel(NetDesc d, float* __restrict__ children, const float* __restrict__
                 const int s0 = 2 * p, s1 = s0 + 1;
                 const bool v1 = s1 < T;
                 const int sl0 = s0 % S, sl1 = v1 ? s1 % S : S;   // slot S: the zero row
-                mbar_wait_sleep(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));
-                if (v1) mbar_wait_sleep(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
+                mbar_wait(&sm.xfull[sl0], (uint32_t)((s0 / S) & 1));   // (x lands early: no sleep hint)
+                if (v1) mbar_wait(&sm.xfull[sl1], (uint32_t)((s1 / S) & 1));
                 const float* xn0 = xring + sl0 * DP + cl;
                 const float* xn1 = xring + sl1 * DP + cl;
                 uint64_t acc0[RW], acc1[RW];
