@@ -153,7 +153,9 @@ pnn_status pnn_create(const int32_t* layers, int32_t n_layers, const int32_t* ac
  * slices (pnn_local_rows says which rows of the full set); pnn_merge finishes
  * with one NCCL all-reduce over the nranks ranks.  nccl_unique_id points to the
  * 128-byte ncclUniqueId every rank received (e.g. via torch.distributed
- * broadcast).  nranks == 1 needs no id (may be NULL) and uses no NCCL.  With
+ * broadcast).  nranks == 1 needs no id: with NULL it uses no NCCL (the fused
+ * local merge); with an id it makes a one-rank communicator and pnn_merge runs
+ * the same partial → ncclAllReduce → finish chain as on N ranks.  With
  * nranks > 1 and id == NULL the rank bookkeeping applies but no communicator
  * is made: the caller reduces itself (pnn_merge_partial → its own all-reduce of
  * the fp64 sums → pnn_merge_finish) and pnn_merge returns PNN_ERR_STATE.  A rank

@@ -390,8 +390,10 @@ pnn_status pnn_set_comm(pnn_net net, const void* id, int32_t nranks, int32_t ran
     net->rank = rank;
     net->k_first = (int)((long long)rank * net->K / nranks);
     net->K_local = (int)((long long)(rank + 1) * net->K / nranks) - net->k_first;
-    if (nranks > 1 && !net->d_msum) CUDA_TRY(net, cudaMalloc(&net->d_msum, sizeof(double) * net->d.P));
-    if (nranks > 1 && id) {                       // id == NULL: the caller reduces (merge_partial/finish)
+    // nranks == 1 with an id still makes a (one-rank) communicator, so the NCCL merge path —
+    // partial sum → ncclAllReduce → finish — runs on a one-GPU box exactly as on eight.
+    if ((nranks > 1 || id) && !net->d_msum) CUDA_TRY(net, cudaMalloc(&net->d_msum, sizeof(double) * net->d.P));
+    if (id) {                                     // id == NULL: the caller reduces (merge_partial/finish)
         std::string why;
         if (!load_nccl(why)) return fail(net, PNN_ERR_NCCL, "%s", why.c_str());
         ncclUniqueId uid;
@@ -623,7 +625,7 @@ pnn_status pnn_merge(pnn_net net, void* stream) {
     CUDA_TRY(net, cudaSetDevice(net->device));
     cudaStream_t cs = (cudaStream_t)stream;
     const long long P = net->d.P;
-    if (net->nranks == 1) {
+    if (net->nranks == 1 && !net->comm) {
         CUDA_TRY(net, launch_merge_local(net->d_children, net->K_local, P, net->K, net->d_merged, cs));
         return PNN_OK;
     }

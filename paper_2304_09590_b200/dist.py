@@ -32,13 +32,16 @@ def rank_rows(N: int, K: int, world: int, rank: int):
 
 def nccl_unique_id_bytes(rank: int, group=None) -> bytes:
     """Create an ncclUniqueId on rank 0 (via torch's NCCL bindings) and broadcast it
-    with torch.distributed; returns the 128 raw bytes on every rank."""
+    with torch.distributed (no process group: a single process, the id as made);
+    returns the 128 raw bytes on every rank."""
     import torch
     import torch.distributed as dist
     if rank == 0:
         uid = bytes(torch.cuda.nccl.unique_id())
     else:
         uid = bytes(128)
+    if not dist.is_initialized():
+        return uid
     obj = [uid]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]

@@ -115,3 +115,23 @@ def test_idle_rank_rejects_rows():
     with pytest.raises(PnnError) as e:
         net.train_epoch(dev(X), dev(y))
     assert e.value.status == 3
+
+
+def test_one_rank_nccl_merge():
+    """pnn_set_comm(1, 0, id) makes a real one-rank NCCL communicator: pnn_merge then runs
+    the multi-rank chain (fp64 partial sum → ncclAllReduce → ÷K, one rounding) on hardware,
+    and must equal the fused local merge and the oracle's merge bit for bit (R18)."""
+    from paper_2304_09590_b200 import PNN
+    from paper_2304_09590_b200.dist import nccl_unique_id_bytes
+    c = CONFIGS["C4"]
+    K = 6
+    X, y = make_split(K * 50 + 5, "train", 0)
+    kids_ref, merged_ref = _single(c, K, X, y)
+    net = PNN(c.layers, c.act, c.init, K, c.lr, seed=0)
+    net.set_comm(1, 0, nccl_unique_id_bytes(0))
+    assert net.local_subnets() == (0, K)
+    net.train_epoch(dev(X), dev(y))
+    net.merge()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(net.get_params(-1), merged_ref)
+    net.close()
