@@ -45,6 +45,10 @@ struct pnn_net_s {
     long long stage_rows = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t stage_released = nullptr;   // recorded after the last launch that reads the staging
+    cudaEvent_t grp_released[8] = {};       // per group of the last host-input call: recorded after
+                                            // the launch that reads that group's staging rows
+    long long grp_n = -1;                   // that call's (n, first CN of this handle's groups,
+    int grp_count = 0, grp_size = 0;        // groups, group size); -1: no per-group record
                                             // buffers (any stream); copy_stream waits on it
     std::vector<float> h_init;        // init parameters (cloned into every CN)
     bool poisoned = false;
@@ -366,6 +370,8 @@ pnn_status pnn_create(const int32_t* layers, int32_t n_layers, const int32_t* ac
             e = cudaMemcpy(net->d_merged, net->h_init.data(), sizeof(float) * d.P, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->stage_released, cudaEventDisableTiming);
+        for (int g = 0; g < 8 && e == cudaSuccess; ++g)
+            e = cudaEventCreateWithFlags(&net->grp_released[g], cudaEventDisableTiming);
         if (e != cudaSuccess)
             st = fail(net, e == cudaErrorMemoryAllocation ? PNN_ERR_OOM : PNN_ERR_CUDA, "%s",
                       cudaGetErrorString(e));
@@ -552,6 +558,7 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         CUDA_TRY(net, cudaMalloc(&net->d_xstage, sizeof(float) * (size_t)n * net->d.n[0]));
         CUDA_TRY(net, cudaMalloc(&net->d_ystage, sizeof(int32_t) * (size_t)n));
         net->stage_rows = n;
+        net->grp_n = -1;
     }
     // Pipeline: the CNs are cut into groups; group g's slices are copied on
     // copy_stream while group g-1 trains on the caller's stream.  A group must still fill
@@ -598,8 +605,15 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         CUDA_TRY(net, cudaEventCreateWithFlags(&guard.ready[g], cudaEventDisableTiming));
         guard.n = g + 1;
     }
-    // the previous call's launches (on any stream) may still read the staging buffers
-    CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, net->stage_released, 0));
+    // The previous call's launches (on any stream) may still read the staging buffers.  When
+    // this call cuts the rows into the same groups as the previous one, group g's copy waits only
+    // for the previous call's group g (same rows; by induction that one waited for the call
+    // before), so the next call's first copies run under the previous call's last wave.
+    // Otherwise every copy waits for all of the previous call's launches.  (The Gram records
+    // are per row too.)
+    const bool per_group = net->grp_n == n && net->grp_count == groups && net->grp_size == gsize;
+    if (!per_group) CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, net->stage_released, 0));
+    net->grp_n = -1;                               // (set again once every group is launched)
     for (int g = 0; g < groups; ++g) {
         const int s0 = g * gsize;
         const int s1 = (g + 1) * gsize < net->K_local ? (g + 1) * gsize : net->K_local;
@@ -607,6 +621,7 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         shard_of(n, net->K_local, s0, &r0, &c0);
         shard_of(n, net->K_local, s1 - 1, &r1, &c1);
         const long long rows = r1 + c1 - r0;
+        if (per_group) CUDA_TRY(net, cudaStreamWaitEvent(net->copy_stream, net->grp_released[g], 0));
         CUDA_TRY(net, cudaMemcpyAsync(net->d_xstage + (size_t)r0 * net->d.n[0], xh + (size_t)r0 * net->d.n[0],
                                       row_bytes * rows, cudaMemcpyHostToDevice, net->copy_stream));
         CUDA_TRY(net, cudaMemcpyAsync(net->d_ystage + r0, yh + r0, sizeof(int32_t) * rows,
@@ -615,7 +630,11 @@ pnn_status pnn_train_epoch_host(pnn_net net, const float* xh, const int32_t* yh,
         CUDA_TRY(net, cudaStreamWaitEvent(cs, guard.ready[g], 0));
         guard.launched = true;
         if ((st = launch_train(net, net->d_xstage, net->d_ystage, n, s0, s1 - s0, cs))) return st;
+        CUDA_TRY(net, cudaEventRecord(net->grp_released[g], cs));   // group g's rows free again
     }
+    net->grp_n = n;
+    net->grp_count = groups;
+    net->grp_size = gsize;
     return PNN_OK;                                 // (the guard waits for the copies)
 }
 
@@ -808,6 +827,8 @@ pnn_status pnn_destroy(pnn_net net) {
     cudaFree(net->d_ystage);
     if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
     if (net->stage_released) cudaEventDestroy(net->stage_released);
+    for (int g = 0; g < 8; ++g)
+        if (net->grp_released[g]) cudaEventDestroy(net->grp_released[g]);
     delete net;
     return PNN_OK;
 }

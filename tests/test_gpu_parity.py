@@ -291,6 +291,25 @@ def test_host_input_path_matches_device_path():
     np.testing.assert_array_equal(a, b)
 
 
+def test_host_input_back_to_back_calls():
+    """Host-input calls issued back to back with different data: each group's staging rows are
+    overwritten only after the previous call's launch that reads them (per-group release when
+    the grouping repeats, a full wait when it changes) — same bits as the device path."""
+    c = CONFIGS["C4"]
+    K = 300                                          # 3 waves of 148 CNs: 3 host-copy groups
+    sets = [make_split(K * 12 + 7, "train", s) for s in (0, 1, 2)] + [make_split(K * 9 + 1, "train", 3)]
+    ref = PNN(c.layers, c.act, c.init, K, c.lr, seed=0)
+    for X, y in sets:
+        ref.train_epoch(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    net = PNN(c.layers, c.act, c.init, K, c.lr, seed=0)
+    pinned = [(torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory()) for X, y in sets]
+    for xh, yh in pinned:
+        net.train_epoch_host(xh, yh)
+    torch.cuda.synchronize()
+    for i in (0, 1, 147, 148, 299):
+        np.testing.assert_array_equal(net.get_params(i), ref.get_params(i))
+
+
 def test_k1_is_snn_and_duplicated_shards(orc):
     """K=1 handle == the sequential network; K CNs on K identical slices stay
     identical and merge back to any one of them (R18)."""
