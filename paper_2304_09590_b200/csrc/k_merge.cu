@@ -3,7 +3,7 @@
 // biases are added onto the PNN … scaled by the number of CNs"; reading R18).
 //
 // HBM-bound: reads K_local·P fp32 once (coalesced: thread i walks child slabs
-// c = 0..K_local-1 at the same offset i), writes P fp32 (or fp64 partials for
+// c = 0..K_local-1 at the same offset i, 16 loads in flight), writes P fp32 (or fp64 partials for
 // the cross-rank all-reduce).  Sums in fp64 in ascending CN order, so K
 // identical clones average back to the clone exactly, then divides by K and
 // rounds once to fp32.
@@ -17,16 +17,14 @@ __device__ __forceinline__ double child_sum(const float* __restrict__ ch, int K_
                                             long long P, long long i) {
     double s = 0.0;
     int c = 0;
-    // 4 independent loads in flight per thread, summed in ascending c order.
-    for (; c + 4 <= K_local; c += 4) {
-        float a = __ldcs(ch + (long long)c * P + i);
-        float b = __ldcs(ch + (long long)(c + 1) * P + i);
-        float e = __ldcs(ch + (long long)(c + 2) * P + i);
-        float f = __ldcs(ch + (long long)(c + 3) * P + i);
-        s += (double)a;
-        s += (double)b;
-        s += (double)e;
-        s += (double)f;
+    // 16 independent loads in flight per thread (one element per thread leaves too few bytes in
+    // flight per SM for HBM otherwise), summed in ascending c order.
+    for (; c + 16 <= K_local; c += 16) {
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = __ldcs(ch + (long long)(c + u) * P + i);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += (double)v[u];
     }
     for (; c < K_local; ++c) s += (double)__ldcs(ch + (long long)c * P + i);
     return s;

@@ -51,6 +51,9 @@ predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restr
                 double acc[KB * TILE];
 #pragma unroll
                 for (int i = 0; i < KB * TILE; ++i) acc[i] = 0.0;
+                // unrolled so each lane has several weight loads in flight (the loop is bound by
+                // their latency, not by the DFMAs)
+#pragma unroll 4
                 for (int j = lane; j < nin; j += 32) {
                     double xv[TILE];
 #pragma unroll
