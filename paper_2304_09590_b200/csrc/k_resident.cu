@@ -113,93 +113,192 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
     return p;
 }
 
+constexpr int GCH = 96;                    // rows per warp chunk (a multiple of the window ring, 6)
+constexpr int GR_SLOTS = 6;                // per-warp shared-memory ring: GR_SLOTS - 1 rows in flight
+constexpr int GR_STRIDE = 800;             // floats per ring slot
+constexpr int GWARPS = 4;                  // warps per CTA
+constexpr size_t kGramSmem = sizeof(float) * GWARPS * GR_SLOTS * GR_STRIDE;
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+template <int N> __device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+struct GramRun {
+    const float* X;
+    const int32_t* Y;
+    float* rec;                             // the records as floats: 8 per row
+    float* ring;                            // this warp's shared-memory ring
+    int D, lane;
+    long long a1, st, nxt_start, base, rem;
+};
+// x(row) into ring slot row % GR_SLOTS: each lane copies exactly the columns it reads back (its
+// own cp.async group), so no cross-lane synchronisation is needed.  One group per call (empty
+// past the chunk end) keeps the wait_group count uniform.
+__device__ __forceinline__ void gram_issue(const GramRun& g, long long row) {
+    if (row < g.a1) {
+        const float* xr = g.X + row * (long long)g.D;
+        float* dst = g.ring + (int)(row % GR_SLOTS) * GR_STRIDE;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) cp_async16(dst + 4 * g.lane + 128 * q, xr + 4 * g.lane + 128 * q);
+        if (4 * g.lane + 768 < g.D) cp_async16(dst + 768 + 4 * g.lane, xr + 768 + 4 * g.lane);
+    }
+    cp_async_commit();
+}
+__device__ __forceinline__ void gram_zero(float4 (&v)[7]) {
+#pragma unroll
+    for (int q = 0; q < 7; ++q) v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ uint64_t gpk(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+// dot(a, b): two f32x2 partial sums over the column pairs, folded
+__device__ __forceinline__ float gdot(const float4 (&a)[7], const float4 (&b)[7]) {
+    uint64_t acc = 0ull;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        acc = ffma2(gpk(a[q].x, a[q].y), gpk(b[q].x, b[q].y), acc);
+        acc = ffma2(gpk(a[q].z, a[q].w), gpk(b[q].z, b[q].w), acc);
+    }
+    float lo, hi;
+    upk(acc, lo, hi);
+    return lo + hi;
+}
+// Row `row` at window phase J: x(row-5+k) is in register buffer (J+k)%6 (k < 5); x(row) is read
+// from the ring into (J+5)%6, which held x(row-6).
+template <int J>
+__device__ __forceinline__ void gram_row(GramRun& g, float4 (&b)[6][7], long long row) {
+    if (row == g.nxt_start) {               // a new slice begins at this row (R17)
+        g.st = row;
+        g.nxt_start += g.base + ((row < g.rem * (g.base + 1)) ? 1 : 0);
+    }
+    cp_async_wait_group<GR_SLOTS - 2>();    // x(row) has landed (this lane's part)
+    {
+        const float* src = g.ring + (int)(row % GR_SLOTS) * GR_STRIDE;
+        float4 (&c)[7] = b[(J + 5) % 6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) c[q] = *reinterpret_cast<const float4*>(src + 4 * g.lane + 128 * q);
+        c[6] = (4 * g.lane + 768 < g.D) ? *reinterpret_cast<const float4*>(src + 768 + 4 * g.lane)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    gram_issue(g, row + GR_SLOTS - 1);      // refills the slot x(row-1) used (consumed last row)
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = gdot(b[(J + k) % 6], b[(J + 5) % 6]);
+    v[5] = v[6] = v[7] = 0.f;
+    // the five dot products reduced together: a transpose-reduce of 8 values over the warp
+    // (lane 4·i ends with the sum of value i: 9 shuffles instead of 5 × 5)
+    const int lane = g.lane;
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    float u4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+    float u2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) u2[i] = (b3 ? u4[i + 2] : u4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? u4[i] : u4[i + 2], 8);
+    float t = (b2 ? u2[1] : u2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? u2[0] : u2[1], 4);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    // record floats [G(u-4), G(u-3), G(u-2), G(u-1), label, G(u-5), 0, 0]; a term that reaches
+    // back past the start of the row's slice is 0
+    if ((lane & 3) == 0) {
+        const int idx = lane >> 2;
+        float val;
+        int pos;
+        if (idx < 5) {
+            val = (row - 5 + idx >= g.st) ? t : 0.f;
+            pos = idx == 0 ? 5 : idx - 1;
+        } else {
+            val = idx == 5 ? __int_as_float(g.Y[row]) : 0.f;
+            pos = idx == 5 ? 4 : idx;
+        }
+        g.rec[8 * row + pos] = val;
+    }
+}
 // Gram record of every row of CNs [s_first, s_first + s_count) (shard-local index u):
 // rec[2·row] = {x(u-4)·x(u), x(u-3)·x(u), x(u-2)·x(u), x(u-1)·x(u)} (0 before the slice
 // start), rec[2·row + 1] = {label bits, x(u-5)·x(u), 0, 0}.  A warp walks a chunk of GCH consecutive
-// rows keeping the last four rows in registers (lane l: columns 4l + 128q, q < 6, and
-// 768 + 4l for l < 4), so X is read from HBM about once.
-constexpr int GCH = 32;
-__global__ void __launch_bounds__(128)
+// rows: x streams through a per-warp shared-memory ring (cp.async, 5 rows in flight), the last
+// five rows stay in registers (lane l: columns 4l + 128q, q < 6, and 768 + 4l for l < 4) as a
+// ring indexed at compile time (the row loop unrolled by 6), each dot product is 14
+// fma.rn.f32x2, so X is read from HBM about once.
+__global__ void __launch_bounds__(GWARPS * 32)
 gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, long long n_local,
             int K_local, int s_first, int s_count, float4* __restrict__ rec) {
+    extern __shared__ __align__(16) float gring[];
     long long r0, c0, r1, c1;
     shard_of(n_local, K_local, s_first, &r0, &c0);
     shard_of(n_local, K_local, s_first + s_count - 1, &r1, &c1);
     const long long rows = r1 + c1 - r0;
     const int lane = threadIdx.x & 31;
     const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-    const long long base = n_local / K_local, rem = n_local % K_local;
-    auto shard_start = [&](long long row) {       // first row of the CN owning `row` (R17)
-        const long long s = (row < rem * (base + 1)) ? row / (base + 1)
-                                                     : rem + (row - rem * (base + 1)) / base;
-        long long st, cnt;
-        shard_of(n_local, K_local, (int)s, &st, &cnt);
-        return st;
-    };
-    auto load = [&](long long row, float4 (&v)[7]) {
-        const float* xr = X + row * (long long)D;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) v[q] = *reinterpret_cast<const float4*>(xr + 4 * lane + 128 * q);
-        v[6] = (4 * lane + 768 < D) ? *reinterpret_cast<const float4*>(xr + 768 + 4 * lane)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-    };
-    auto dot = [](const float4 (&a)[7], const float4 (&b)[7]) {
-        float s = 0.f;
-#pragma unroll
-        for (int q = 0; q < 7; ++q)
-            s = fmaf(a[q].w, b[q].w, fmaf(a[q].z, b[q].z, fmaf(a[q].y, b[q].y, fmaf(a[q].x, b[q].x, s))));
-        return s;
-    };
+    GramRun g;
+    g.X = X; g.Y = Y; g.rec = reinterpret_cast<float*>(rec); g.D = D; g.lane = lane;
+    g.ring = gring + (threadIdx.x >> 5) * (GR_SLOTS * GR_STRIDE);
+    g.base = n_local / K_local;
+    g.rem = n_local % K_local;
     const long long nchunks = (rows + GCH - 1) / GCH;
     for (long long ch = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
-        const long long a0 = r0 + ch * GCH, a1 = min(a0 + GCH, r0 + rows);
-        float4 win[5][7];                          // win[k] = x(row - 5 + k)
-        const long long st = shard_start(a0);
-        // the next slice boundary after a0 (no per-row division: the rows are walked in order)
-        long long nxt_start;
-        {
-            const long long sidx = (a0 < rem * (base + 1)) ? a0 / (base + 1) : rem + (a0 - rem * (base + 1)) / base;
-            long long s1, c1;
-            shard_of(n_local, K_local, (int)sidx, &s1, &c1);
-            nxt_start = s1 + c1;
-        }
+        const long long a0 = r0 + ch * GCH;
+        g.a1 = min(a0 + GCH, r0 + rows);
+        cp_async_wait_all();                   // the previous chunk's (empty) groups
+#pragma unroll
+        for (int k = 0; k < GR_SLOTS - 1; ++k) gram_issue(g, a0 + k);
+        // the slice holding a0: its start (window rows before it are not loaded) and the next
+        const long long sidx = (a0 < g.rem * (g.base + 1)) ? a0 / (g.base + 1)
+                                                           : g.rem + (a0 - g.rem * (g.base + 1)) / g.base;
+        long long s1, cnt;
+        shard_of(n_local, K_local, (int)sidx, &s1, &cnt);
+        g.st = s1;
+        g.nxt_start = s1 + cnt;
+        float4 b[6][7];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
             const long long pr = a0 - 5 + k;
-            if (pr >= st) load(pr, win[k]);
-            else
+            if (pr >= g.st) {
+                const float* xr = X + pr * (long long)D;
 #pragma unroll
-                for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        float4 nxt[7];
-        load(a0, nxt);
-        for (long long row = a0; row < a1; ++row) {
-            if (row == nxt_start) {                // a new slice begins: no terms before it
-#pragma unroll
-                for (int k = 0; k < 5; ++k)
-#pragma unroll
-                    for (int q = 0; q < 7; ++q) win[k][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                nxt_start += base + ((row < rem * (base + 1)) ? 1 : 0);   // R17: slices before rem are base+1 long
+                for (int q = 0; q < 6; ++q) b[k][q] = *reinterpret_cast<const float4*>(xr + 4 * lane + 128 * q);
+                b[k][6] = (4 * lane + 768 < D) ? *reinterpret_cast<const float4*>(xr + 768 + 4 * lane)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                gram_zero(b[k]);
             }
-            float4 cur[7];
-#pragma unroll
-            for (int q = 0; q < 7; ++q) cur[q] = nxt[q];
-            if (row + 1 < a1) load(row + 1, nxt);  // one row ahead
-            float gk[5];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) gk[k] = warp_sum(dot(win[k], cur));
-            if (lane == 0) {                       // {G(u-4..u-1)}, {label, G(u-5)} (the paired sweeps' 5th term)
-                rec[2 * row] = make_float4(gk[1], gk[2], gk[3], gk[4]);
-                rec[2 * row + 1] = make_float4(__int_as_float(Y[row]), gk[0], 0.f, 0.f);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int q = 0; q < 7; ++q) win[k][q] = win[k + 1][q];
-#pragma unroll
-            for (int q = 0; q < 7; ++q) win[4][q] = cur[q];
         }
+        // (rows are uniform over the warp; GCH is a multiple of 6, only the last chunk is short)
+        const long long n6 = (g.a1 - a0) / 6;
+        long long row = a0;
+        for (long long i = 0; i < n6; ++i, row += 6) {
+            gram_row<0>(g, b, row);
+            gram_row<1>(g, b, row + 1);
+            gram_row<2>(g, b, row + 2);
+            gram_row<3>(g, b, row + 3);
+            gram_row<4>(g, b, row + 4);
+            gram_row<5>(g, b, row + 5);
+        }
+        const int left = (int)(g.a1 - row);
+        if (left > 0) gram_row<0>(g, b, row);
+        if (left > 1) gram_row<1>(g, b, row + 1);
+        if (left > 2) gram_row<2>(g, b, row + 2);
+        if (left > 3) gram_row<3>(g, b, row + 3);
+        if (left > 4) gram_row<4>(g, b, row + 4);
     }
+    cp_async_wait_all();
+}
+
+// Launch of the Gram pre-pass (its shared-memory ring needs the opt-in size once).
+cudaError_t gram_launch(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
+                        int s_count, float4* rec, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    gram_kernel<<<148 * 2, GWARPS * 32, kGramSmem, st>>>(x, labels, D, n_local, K_local, s_first, s_count, rec);
+    return cudaGetLastError();
 }
 
 template <int C, int A1, int A2, bool TRACE>
@@ -1118,8 +1217,7 @@ cudaError_t launch_c(const ResidentPlan& p, const NetDesc& d, float* children, c
 cudaError_t launch_gram(const float* x, const int32_t* labels, int D, long long n_local, int K_local, int s_first,
                         int s_count, float4* rec, cudaStream_t st) {
     if (s_count <= 0) return cudaSuccess;
-    gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, D, n_local, K_local, s_first, s_count, rec);
-    return cudaGetLastError();
+    return gram_launch(x, labels, D, n_local, K_local, s_first, s_count, rec, st);
 }
 
 ResidentPlan plan_resident(const NetDesc& d, int batch, int concurrent, int variant) {
@@ -1208,8 +1306,7 @@ cudaError_t launch_sgd_resident(const ResidentPlan& p, const NetDesc& d, float* 
         if (e != cudaSuccess || !ev1) return e;
         return cudaEventRecord(ev1, st);
     }
-    gram_kernel<<<148 * 4, 128, 0, st>>>(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec);
-    e = cudaGetLastError();
+    e = gram_launch(x, labels, d.n[0], n_local, K_local, s_first, s_count, rec, st);
     if (e != cudaSuccess) return e;
     if (ev0) {                                     // timing hook: bracket the SGD launch only
         if ((e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
