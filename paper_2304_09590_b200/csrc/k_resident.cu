@@ -113,7 +113,7 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
     return p;
 }
 
-constexpr int GCH = 96;                    // rows per warp chunk (a multiple of the window ring, 6)
+constexpr int GCH = 96;                    // least rows per warp chunk (a multiple of the window ring, 6)
 constexpr int GR_SLOTS = 6;                // per-warp shared-memory ring: GR_SLOTS - 1 rows in flight
 constexpr int GR_STRIDE = 800;             // floats per ring slot
 constexpr int GWARPS = 4;                  // warps per CTA
@@ -219,8 +219,8 @@ __device__ __forceinline__ void gram_row(GramRun& g, float4 (&b)[6][7], long lon
 }
 // Gram record of every row of CNs [s_first, s_first + s_count) (shard-local index u):
 // rec[2·row] = {x(u-4)·x(u), x(u-3)·x(u), x(u-2)·x(u), x(u-1)·x(u)} (0 before the slice
-// start), rec[2·row + 1] = {label bits, x(u-5)·x(u), 0, 0}.  A warp walks a chunk of GCH consecutive
-// rows: x streams through a per-warp shared-memory ring (cp.async, 5 rows in flight), the last
+// start), rec[2·row + 1] = {label bits, x(u-5)·x(u), 0, 0}.  A warp walks a chunk of consecutive
+// rows (rows / warps of them, at least GCH): x streams through a per-warp shared-memory ring (cp.async, 5 rows in flight), the last
 // five rows stay in registers (lane l: columns 4l + 128q, q < 6, and 768 + 4l for l < 4) as a
 // ring indexed at compile time (the row loop unrolled by 6), each dot product is 14
 // fma.rn.f32x2, so X is read from HBM about once.
@@ -239,10 +239,14 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
     g.ring = gring + (threadIdx.x >> 5) * (GR_SLOTS * GR_STRIDE);
     g.base = n_local / K_local;
     g.rem = n_local % K_local;
-    const long long nchunks = (rows + GCH - 1) / GCH;
+    // one contiguous chunk per warp when the rows allow it (no last partial round of chunks, the
+    // 5 window rows re-read once per warp), never shorter than GCH rows
+    long long gch = (rows + nwarps - 1) / nwarps;
+    gch = max((gch + 5) / 6 * 6, (long long)GCH);
+    const long long nchunks = (rows + gch - 1) / gch;
     for (long long ch = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
-        const long long a0 = r0 + ch * GCH;
-        g.a1 = min(a0 + GCH, r0 + rows);
+        const long long a0 = r0 + ch * gch;
+        g.a1 = min(a0 + gch, r0 + rows);
         cp_async_wait_all();                   // the previous chunk's (empty) groups
 #pragma unroll
         for (int k = 0; k < GR_SLOTS - 1; ++k) gram_issue(g, a0 + k);
@@ -267,7 +271,7 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
                 gram_zero(b[k]);
             }
         }
-        // (rows are uniform over the warp; GCH is a multiple of 6, only the last chunk is short)
+        // (rows are uniform over the warp; the chunk length is a multiple of 6, only the last chunk is short)
         const long long n6 = (g.a1 - a0) / 6;
         long long row = a0;
         for (long long i = 0; i < n6; ++i, row += 6) {
