@@ -114,7 +114,8 @@ template <typename T> __device__ __forceinline__ T* opaque(T* p) {
 }
 
 constexpr int GCH = 96;                    // least rows per warp chunk (a multiple of the window ring, 6)
-constexpr int GR_SLOTS = 6;                // per-warp shared-memory ring: GR_SLOTS - 1 rows in flight
+constexpr int GR_SLOTS = 6;                // per-warp shared-memory ring (= the register window ring, so the slot of
+                                           // a row is a compile-time constant in the unrolled loop): 5 rows in flight
 constexpr int GR_STRIDE = 800;             // floats per ring slot
 constexpr int GWARPS = 4;                  // warps per CTA
 constexpr size_t kGramSmem = sizeof(float) * GWARPS * GR_SLOTS * GR_STRIDE;
@@ -130,15 +131,18 @@ struct GramRun {
     float* rec;                             // the records as floats: 8 per row
     float* ring;                            // this warp's shared-memory ring
     int D, lane;
+    int ynext;                              // label of the next row, loaded one row ahead
     long long a1, st, nxt_start, base, rem;
 };
-// x(row) into ring slot row % GR_SLOTS: each lane copies exactly the columns it reads back (its
-// own cp.async group), so no cross-lane synchronisation is needed.  One group per call (empty
-// past the chunk end) keeps the wait_group count uniform.
-__device__ __forceinline__ void gram_issue(const GramRun& g, long long row) {
+// x(row) into ring slot `slot` (= (row - chunk start) % GR_SLOTS, a compile-time constant at
+// the call sites of the unrolled row loop: a 64-bit row % 6 costs more than the row's dot
+// products): each lane copies exactly the columns it reads back (its own cp.async group), so
+// no cross-lane synchronisation is needed.  One group per call (empty past the chunk end)
+// keeps the wait_group count uniform.
+__device__ __forceinline__ void gram_issue(const GramRun& g, long long row, int slot) {
     if (row < g.a1) {
         const float* xr = g.X + row * (long long)g.D;
-        float* dst = g.ring + (int)(row % GR_SLOTS) * GR_STRIDE;
+        float* dst = g.ring + slot * GR_STRIDE;
 #pragma unroll
         for (int q = 0; q < 6; ++q) cp_async16(dst + 4 * g.lane + 128 * q, xr + 4 * g.lane + 128 * q);
         if (4 * g.lane + 768 < g.D) cp_async16(dst + 768 + 4 * g.lane, xr + 768 + 4 * g.lane);
@@ -174,16 +178,20 @@ __device__ __forceinline__ void gram_row(GramRun& g, float4 (&b)[6][7], long lon
         g.st = row;
         g.nxt_start += g.base + ((row < g.rem * (g.base + 1)) ? 1 : 0);
     }
+    // the label rides one row ahead: loaded where it is stored, the row's record store would wait
+    // a whole L2 round trip on it
+    const int ylab = g.ynext;
+    if (row + 1 < g.a1) g.ynext = g.Y[row + 1];
     cp_async_wait_group<GR_SLOTS - 2>();    // x(row) has landed (this lane's part)
     {
-        const float* src = g.ring + (int)(row % GR_SLOTS) * GR_STRIDE;
+        const float* src = g.ring + J * GR_STRIDE;
         float4 (&c)[7] = b[(J + 5) % 6];
 #pragma unroll
         for (int q = 0; q < 6; ++q) c[q] = *reinterpret_cast<const float4*>(src + 4 * g.lane + 128 * q);
         c[6] = (4 * g.lane + 768 < g.D) ? *reinterpret_cast<const float4*>(src + 768 + 4 * g.lane)
                                         : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    gram_issue(g, row + GR_SLOTS - 1);      // refills the slot x(row-1) used (consumed last row)
+    gram_issue(g, row + GR_SLOTS - 1, (J + GR_SLOTS - 1) % GR_SLOTS);   // refills the slot x(row-1) used (consumed last row)
     float v[8];
 #pragma unroll
     for (int k = 0; k < 5; ++k) v[k] = gdot(b[(J + k) % 6], b[(J + 5) % 6]);
@@ -211,7 +219,7 @@ __device__ __forceinline__ void gram_row(GramRun& g, float4 (&b)[6][7], long lon
             val = (row - 5 + idx >= g.st) ? t : 0.f;
             pos = idx == 0 ? 5 : idx - 1;
         } else {
-            val = idx == 5 ? __int_as_float(g.Y[row]) : 0.f;
+            val = idx == 5 ? __int_as_float(ylab) : 0.f;
             pos = idx == 5 ? 4 : idx;
         }
         g.rec[8 * row + pos] = val;
@@ -249,7 +257,8 @@ gram_kernel(const float* __restrict__ X, const int32_t* __restrict__ Y, int D, l
         g.a1 = min(a0 + gch, r0 + rows);
         cp_async_wait_all();                   // the previous chunk's (empty) groups
 #pragma unroll
-        for (int k = 0; k < GR_SLOTS - 1; ++k) gram_issue(g, a0 + k);
+        for (int k = 0; k < GR_SLOTS - 1; ++k) gram_issue(g, a0 + k, k);
+        g.ynext = Y[a0];
         // the slice holding a0: its start (window rows before it are not loaded) and the next
         const long long sidx = (a0 < g.rem * (g.base + 1)) ? a0 / (g.base + 1)
                                                            : g.rem + (a0 - g.rem * (g.base + 1)) / g.base;
