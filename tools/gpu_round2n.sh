@@ -1,5 +1,7 @@
 #!/bin/bash
-# Round-2 batch (n): Gram pre-pass chunking / ring-depth A/B (tools-only variant builds), parity on the new chunking.
+# Round-2 batch (n): Gram pre-pass chunking / ring-depth A/B, parity on the new chunking. The gfix / gs4 / gs8 libraries were
+# experiment-only builds (-DPNN_GRAM_FIXED_CHUNK, -DPNN_GRAM_SLOTS=4|8); those switches were removed after the A/B
+# (results: profiles/README.md, r2r), so this script documents the run and no longer reproduces it.
 cd "$(dirname "$0")/.." || exit 1
 O=gpurun_out/r2n; mkdir -p $O
 B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e"
