@@ -30,9 +30,36 @@ predict_kernel(NetDesc d, const float* __restrict__ params, const float* __restr
     double* xin = smd + 2 * (size_t)TILE * Hm;                 // [TILE][n0] inputs, converted once
     for (long long t0 = (long long)blockIdx.x * TILE; t0 < n; t0 += (long long)gridDim.x * TILE) {
         const int nt = (int)((n - t0) < TILE ? (n - t0) : TILE);
-        for (int i = tid; i < TILE * n0; i += kThreads) {
-            int s = i / n0, j = i % n0;
-            xin[i] = (s < nt) ? (double)X[(t0 + s) * n0 + j] : 0.0;
+        if ((n0 & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+            // 16-byte loads, all of a thread's loads issued before the first conversion (one DRAM
+            // round trip per tile instead of one per unrolled group of scalar loads)
+            const int n4 = n0 >> 2;
+            constexpr int kMaxV = 4;                       // float4 loads in flight per thread
+            for (int i0 = tid; i0 < TILE * n4; i0 += kMaxV * kThreads) {
+                float4 v[kMaxV];
+#pragma unroll
+                for (int u = 0; u < kMaxV; ++u) {
+                    const int i = i0 + u * kThreads;
+                    const int s = i / n4, j4 = i - s * n4;
+                    v[u] = (i < TILE * n4 && s < nt)
+                               ? *reinterpret_cast<const float4*>(X + (t0 + s) * n0 + 4 * j4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < kMaxV; ++u) {
+                    const int i = i0 + u * kThreads;
+                    if (i < TILE * n4) {
+                        double2* dst = reinterpret_cast<double2*>(xin + 4 * (size_t)i);
+                        dst[0] = make_double2((double)v[u].x, (double)v[u].y);
+                        dst[1] = make_double2((double)v[u].z, (double)v[u].w);
+                    }
+                }
+            }
+        } else {
+            for (int i = tid; i < TILE * n0; i += kThreads) {
+                int s = i / n0, j = i % n0;
+                xin[i] = (s < nt) ? (double)X[(t0 + s) * n0 + j] : 0.0;
+            }
         }
         __syncthreads();
         const double* inD = nullptr;
