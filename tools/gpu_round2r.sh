@@ -2,7 +2,7 @@
 # Round-2 closing batch (r) on the final build (Gram pre-pass 0.547 ms): smoke, the default C4 bench line, the full
 # GPU suite, the C4 launch list, ncu full captures of the v12 SGD launch and the Gram pre-pass.
 cd "$(dirname "$0")/.." || exit 1
-O=gpurun_out/r2r; mkdir -p $O
+O=gpurun_out/${1:-r2r}; mkdir -p $O
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
 timeout 900 python bench.py > $O/bench_C4.json 2> $O/bench_C4.err; echo "bench C4 rc=$?"
 timeout 600 python bench.py --config C3 --steps 3 --warmup 3 > $O/bench_C3.json 2> $O/bench_C3.err; echo "bench C3 rc=$?"
